@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""bench.py — microstructure point-updates/s (fp64) on B200.
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+N = 2^20 points on a 128x128x64 lattice, 10,000 explicit steps of dt = 2e-5 s,
+temperatures from the on-device Rosenthal raster generator,
+initial state (0.9, 0, 0.1).  One bench "step" = that whole job: 10,000
+time steps over all 2^20 points (1.05e10 point-updates), run by the fused
+advance kernel (K2) in 10 launches of 1,000 steps with phase sums after each.
+Weak scaling: each rank runs its own copy of the job (one GPU per rank).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+`--impl reference` times the reference's CPU algorithm (the C oracle port,
+oracle/ti64_oracle.c, OpenMP over all host cores) on the same workload and
+prints the same JSON line with "impl": "reference".
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "microstructure point-updates/s (fp64)"
+UNIT = "point-updates/s"
+JOB_STEPS = 10_000
+SNAP_EVERY = 1_000
+WORKLOAD = ("config1: Rosenthal raster (200 W, eta 0.35, 1 m/s, 100 um hatch), "
+            "N=2^20 points on 128x128x64 lattice h=20um, 10000 steps dt=2e-5 s, "
+            "state (0.9,0,0.1)")
+# Algorithmic flops per point-update (bench.py:45-58 counts):
+# F = 48 + 22[T1<848] + 46[grow|am] + 49[grow] + 49[am] + 98[dissolve] + 18
+F_BASE, F_FORM, F_GA, F_GROW, F_AM, F_DIS, F_TAIL = 48, 22, 46, 49, 49, 98, 18
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                s, m = float(p[1]), float(p[2])
+            except ValueError:
+                continue
+            sm.append(s)
+            smax = max(smax, m)
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flops_from_totals(t):
+    return (F_BASE + F_TAIL) * t["point_updates"] + F_FORM * t["n_form"] + \
+        F_GA * t["n_grow_or_am"] + F_GROW * t["n_grow"] + F_AM * t["n_am"] + \
+        F_DIS * t["n_dissolve"]
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline: the C oracle (port of the reference
+# algorithm) on the box's host cores.
+# ---------------------------------------------------------------------------
+
+def cpu_reference(budget_s=12.0, max_steps=JOB_STEPS, threads=None):
+    """Time the oracle's step_all (lanes=8, all host threads) on config 1.
+    Temperatures are generated per step outside the timed region."""
+    from oracle import oracle as orc
+    from paper_2402_17580_b200 import sources
+    from paper_2402_17580_b200.kinetics import DEFAULT_PARAMS
+    from paper_2402_17580_b200.integrator import IntegratorConfig
+    threads = threads or os.cpu_count() or 1
+    src = sources.source_for_config(1)
+    n = src.n_points
+    tab = src.beam_table(max_steps + 1)
+    g = src.tempgen(0, tab.ctypes.data, len(tab))
+    f = orc.gen_initial_state(g, n)
+    f.temperature_old[:] = orc.gen_temperature(g, n, 0, threads)
+    kp = DEFAULT_PARAMS.kernel_tuple()
+    cfg = IntegratorConfig().kernel_tuple()
+    # warm-up (first touch, thread pool)
+    f.temperature_new[:] = orc.gen_temperature(g, n, 1, threads)
+    w = f.copy()
+    orc.step_all(w, src.dt, kp, cfg, n_lanes=8, threads=threads)
+    timed, steps = 0.0, 0
+    while steps < max_steps and timed < budget_s:
+        f.temperature_new[:] = orc.gen_temperature(g, n, steps + 1, threads)
+        t0 = time.perf_counter()
+        orc.step_all(f, src.dt, kp, cfg, n_lanes=8, threads=threads)
+        timed += time.perf_counter() - t0
+        steps += 1
+    ups = n * steps / timed
+    return {"value": ups, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"config-1 lattice, all {n} points x first {steps} of {JOB_STEPS} "
+                      f"steps, oracle step_all (lanes=8, OpenMP {threads} threads), "
+                      f"T generated outside the timed region; {timed:.1f} s timed",
+            "seconds": timed}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    base = cpu_reference(budget_s=max(2.0, 2.0 * args.steps))
+    line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "points": 1 << 20,
+                       "note": "CPU: bounded sample of the same job"},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def measure_fp64_peak(torch, lib, stream):
+    import ctypes as C
+    from paper_2402_17580_b200 import _lib
+    sc = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks = 148 * 8
+    best = 0.0
+    h = C.c_void_p(stream.cuda_stream)
+    for it in (2000, 20000, 20000, 20000):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fl = lib.ti64_bench_dfma(_lib.ptr(sc), it, blocks, h)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        if it > 2000:
+            best = max(best, fl / (ms * 1e-3))
+    return best
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2402_17580_b200 as pkg
+    from paper_2402_17580_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.require()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    src = pkg.source_for_config(1)
+    n = src.n_points
+    nsteps = args.job_steps
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    pristine = pkg.init_from_source(src, n, device=dev)
+    work = pristine.copy()
+    scratch = pkg.batch._scratch(n, dev)
+
+    def one_job(fields, counters=None):
+        return pkg.advance(fields, nsteps, src, snapshot_every=SNAP_EVERY,
+                           counters=counters, scratch=scratch)
+
+    # warm-up
+    for _ in range(args.warmup):
+        for k in pkg.batch.NAMES:
+            getattr(work, k).copy_(getattr(pristine, k))
+        one_job(work)
+    torch.cuda.synchronize()
+
+    # flop model totals of the job (deterministic; one counted run, untimed)
+    for k in pkg.batch.NAMES:
+        getattr(work, k).copy_(getattr(pristine, k))
+    cnt = pkg.EventCounters(n, dev)
+    one_job(work, cnt)
+    totals = cnt.totals_dict()
+    flops_job = flops_from_totals(totals)
+    counted_state = work.to_host()
+
+    # timed region
+    times = []
+    launches = 0
+    sums_last = None
+    with ClockSampler(local) as clk:
+        barrier()
+        for _ in range(args.steps):
+            for k in pkg.batch.NAMES:
+                getattr(work, k).copy_(getattr(pristine, k))
+            flush.fill_(1.0)  # > L2: evict the previous job's state
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = one_job(work)
+            e1.record(stream)
+            launches += r.launches
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e-3)
+            sums_last = r.sums
+        barrier()
+    # uncounted timed run must reproduce the counted run bit for bit
+    same = all(np.array_equal(work.host(k), counted_state[k]) for k in pkg.batch.NAMES)
+    total_s = sum(times)
+    t_max = torch.tensor([total_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        # final global phase-fraction reduction (the path's only exchange)
+        dist.all_reduce(sums_last, op=dist.ReduceOp.SUM)
+    total_s = float(t_max.item())
+    upd_job = n * nsteps
+    value = world * upd_job * args.steps / total_s
+
+    # e2e through the public API: pinned host inputs -> H2D, advance, D2H states
+    host = {k: torch.from_numpy(pristine.host(k)).pin_memory() for k in pkg.batch.NAMES}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier()
+        t0 = time.perf_counter()
+        f = pkg.GlobalFields(*[host[k] for k in pkg.batch.NAMES], device=dev)
+        pkg.advance(f, nsteps, src, snapshot_every=SNAP_EVERY, scratch=scratch)
+        st = f.states()
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    d2h = st.nbytes
+    e2e_t = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * upd_job / float(e2e_t.item())
+
+    if rank == 0:
+        peak = measure_fp64_peak(torch, lib, stream)
+        per_launch_s = total_s / (args.steps * (nsteps // SNAP_EVERY))
+        flops_launch = flops_job / (nsteps // SNAP_EVERY)
+        achieved = flops_launch / per_launch_s / 1e12
+        peak_tf = peak / 1e12
+        cpu = None if args.no_cpu_baseline else cpu_reference(budget_s=args.cpu_budget)
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "points_per_gpu": n, "job_steps": nsteps,
+                       "snapshot_every": SNAP_EVERY,
+                       "l2": "flushed between timed iterations (256 MiB write)",
+                       "parallelism": f"points sharded, {world} replica(s) of the job"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf,
+                         "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": None,
+                         "peak_source": "measured on this box: DFMA stream (ti64_bench_dfma)",
+                         "flops_per_update": flops_job / upd_job,
+                         "kernel": "advance_kernel<ROSENTHAL>"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "cpu_baseline": None if cpu is None else
+            {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "checks": {"counted_equals_timed_bitwise": bool(same),
+                       "sums_last": [float(x) for x in sums_last[-1].cpu().numpy()],
+                       "totals": totals},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--job-steps", type=int, default=JOB_STEPS)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

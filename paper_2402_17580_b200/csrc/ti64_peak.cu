@@ -1,0 +1,47 @@
+// ti64_peak.cu — FP64 roofline denominator: a dependent-free DFMA stream.
+// MEASURED_PEAKS.json carries no FP64 figure, so bench.py measures it on
+// the box with this kernel (8 independent FMA chains per thread, full
+// occupancy, 148 SMs) and reports the roofline fraction "of measured".
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/ti64_b200.h"
+
+void ti64_set_error(const std::string& msg);
+
+namespace {
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, int64_t iters, double b,
+                                                  double c) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-3, a2 = a0 + 2e-3, a3 = a0 + 3e-3;
+  double a4 = a0 + 4e-3, a5 = a0 + 5e-3, a6 = a0 + 6e-3, a7 = a0 + 7e-3;
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = __fma_rn(a0, b, c); a1 = __fma_rn(a1, b, c); a2 = __fma_rn(a2, b, c);
+      a3 = __fma_rn(a3, b, c); a4 = __fma_rn(a4, b, c); a5 = __fma_rn(a5, b, c);
+      a6 = __fma_rn(a6, b, c); a7 = __fma_rn(a7, b, c);
+    }
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+extern "C" int64_t ti64_bench_dfma(double* scratch_d, int64_t iters, int32_t blocks,
+                                   void* stream) {
+  if (!scratch_d || iters < 1 || blocks < 1) {
+    ti64_set_error("ti64_bench_dfma: bad argument");
+    return TI64_EINVAL;
+  }
+  dfma_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      scratch_d, iters, 0.9999999999, 1e-12);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ti64_set_error(std::string("ti64_bench_dfma: ") + cudaGetErrorString(e));
+    return TI64_ECUDA;
+  }
+  // flops per launch: blocks * 256 threads * iters * 4 * 8 FMAs * 2
+  return (int64_t)blocks * 256 * iters * 64;
+}

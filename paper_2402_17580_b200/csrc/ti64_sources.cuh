@@ -1,0 +1,190 @@
+// ti64_sources.cuh — on-device seeded temperature-history generators (K3).
+//
+// Definitions are shared bit for bit with the checker in
+// oracle/ti64_oracle.c (oracle_gen_temperature1).  Per-point parameters come
+// from a counter-based splitmix64 hash of (seed, global point index, draw),
+// so a point's history does not depend on sharding or launch shape.
+//
+// Pulse sums skip pulses whose contribution is provably an exact no-op:
+// outside a conservative step window around its centre u^2 > 45, so
+// A*fast_exp(-u^2) < 1e-16 while the running sum is >= base >= 256, whose
+// half-ulp is 2^-45 ~ 2.8e-14 — adding it cannot change a bit.
+#pragma once
+#include "ti64_fastmath.cuh"
+#include "../../include/ti64_b200.h"
+
+namespace ti64 {
+
+__host__ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ double u01(uint64_t seed, uint64_t point, uint64_t k) {
+  const uint64_t b = splitmix(splitmix(seed ^ splitmix(point)) ^ (k * 0xD1B54A32D192ED03ULL));
+  return __dmul_rn(__ull2double_rn(b >> 11), 0x1.0p-53);
+}
+
+__device__ __forceinline__ double unif(double lo, double hi, double u) {
+  return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u));
+}
+
+// (double)n exactly, n in [0, 2^52): one DADD instead of an I2F conversion
+__device__ __forceinline__ double step_to_double(int64_t n) {
+  return __dsub_rn(__hiloint2double(0x43300000 | (int)(n >> 32), (int)(uint32_t)n),
+                   4503599627370496.0);
+}
+
+// Gaussian pulse contribution a*fast_exp(-u^2), u = (t - tc)*inv_w.
+// -u*u is never NaN and <= 0; below -708 fast_exp is exactly 0.
+__device__ __forceinline__ double add_pulse(double s, double a, double tc, double inv_w,
+                                            double t) {
+  const double u = __dmul_rn(__dsub_rn(t, tc), inv_w);
+  const double uu = __dmul_rn(u, u);
+  if (uu > 708.0) return __dadd_rn(s, 0.0);  // a * 0.0 == +0.0
+  return __dadd_rn(s, __dmul_rn(a, exp_core(-uu)));
+}
+
+// Up to MAXP Gaussian pulses per point (configs 0, 2, 4).  Pulse k is only
+// evaluated on steps [lo_k, hi_k]; a live mask plus the next step at which
+// it changes keep the per-step cost at the live pulses.
+template <int MAXP>
+struct PulseSet {
+  double base;
+  double a[MAXP], tc[MAXP], inv_w[MAXP];
+  int lo[MAXP], hi[MAXP];
+  int np;
+  unsigned live;
+  int64_t next_event;
+
+  __device__ __forceinline__ void add(int k, double ak, double tck, double w, double dt) {
+    a[k] = ak;
+    tc[k] = tck;
+    inv_w[k] = __ddiv_rn(1.0, w);
+    // conservative window: outside it |t - tc| >= 7w - O(ulp) => u^2 > 45
+    const double l = floor((tck - 7.0 * w) / dt) - 2.0;
+    const double h = ceil((tck + 7.0 * w) / dt) + 2.0;
+    lo[k] = l < -1.0e9 ? -1000000000 : (l > 1.0e9 ? 1000000000 : (int)l);
+    hi[k] = h < -1.0e9 ? -1000000000 : (h > 1.0e9 ? 1000000000 : (int)h);
+  }
+
+  __device__ __forceinline__ void rescan(int64_t n) {
+    live = 0u;
+    int64_t nxt = INT64_MAX;
+    for (int k = 0; k < np; ++k) {
+      if (n >= lo[k] && n <= hi[k]) {
+        live |= 1u << k;
+        nxt = min(nxt, (int64_t)hi[k] + 1);
+      } else if (n < lo[k]) {
+        nxt = min(nxt, (int64_t)lo[k]);
+      }
+    }
+    next_event = nxt;
+  }
+
+  __device__ __forceinline__ double temp(int64_t n, double t) {
+    if (n >= next_event || n < 0) rescan(n);
+    double s = base;
+    unsigned m = live;
+    while (m) {
+      const int k = __ffs(m) - 1;
+      m &= m - 1;
+      s = add_pulse(s, a[k], tc[k], inv_w[k], t);
+    }
+    return s;
+  }
+};
+
+// config 0 (TI64_SRC_PULSE): p = {A_lo, A_hi, tc_lo, tc_hi, w_lo, w_hi}
+template <int MAXP>
+__device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempgen& g,
+                                            uint64_t pt) {
+  ps.base = g.base;
+  ps.np = 1;
+  const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
+  const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 1));
+  const double w = unif(g.p[4], g.p[5], u01(g.seed, pt, 2));
+  ps.add(0, a, tc, w, g.dt);
+  ps.next_event = -1;
+  ps.live = 0u;
+}
+
+// config 2 (TI64_SRC_PULSE_TRAIN): p = {A1_lo, A1_hi, j_lo, j_hi, t0, spacing,
+// tj_lo, tj_hi, w_lo, w_hi, decay, xs_lo, xs_hi}
+template <int MAXP>
+__device__ __forceinline__ void init_train(PulseSet<MAXP>& ps, const ti64_tempgen& g,
+                                           uint64_t pt) {
+  ps.base = g.base;
+  ps.np = g.max_pulses < MAXP ? g.max_pulses : MAXP;
+  const double a1 = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
+  double scale = 1.0;
+  for (int k = 0; k < ps.np; ++k) {
+    const double a = __dmul_rn(__dmul_rn(a1, scale), unif(g.p[2], g.p[3], u01(g.seed, pt, 1 + 3 * k)));
+    const double tc = __dadd_rn(__dadd_rn(g.p[4], __dmul_rn(g.p[5], (double)k)),
+                                unif(g.p[6], g.p[7], u01(g.seed, pt, 2 + 3 * k)));
+    const double w = unif(g.p[8], g.p[9], u01(g.seed, pt, 3 + 3 * k));
+    ps.add(k, a, tc, w, g.dt);
+    scale = __dmul_rn(scale, g.p[10]);
+  }
+  ps.next_event = -1;
+  ps.live = 0u;
+}
+
+// config 4 (TI64_SRC_PULSE_SWEEP): p = {A_lo, A_hi, c_lo, c_hi, lnw_lo, lnw_hi}
+template <int MAXP>
+__device__ __forceinline__ void init_sweep(PulseSet<MAXP>& ps, const ti64_tempgen& g,
+                                           uint64_t pt) {
+  ps.base = g.base;
+  int np_ = 1 + (int)__dmul_rn(u01(g.seed, pt, 0), (double)g.max_pulses);
+  ps.np = np_ < MAXP ? np_ : MAXP;
+  for (int k = 0; k < ps.np; ++k) {
+    const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 1 + 3 * k));
+    const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 2 + 3 * k));
+    const double w = fast_exp(unif(g.p[4], g.p[5], u01(g.seed, pt, 3 + 3 * k)));
+    ps.add(k, a, tc, w, g.dt);
+  }
+  ps.next_event = -1;
+  ps.live = 0u;
+}
+
+// config 1 (TI64_SRC_ROSENTHAL): p = {coef, v/(2 alpha), cap}
+struct Rosenthal {
+  double x, y, dd, base, coef, vk, cap;
+  const double* beam;
+
+  __device__ __forceinline__ void init(const ti64_tempgen& g, uint64_t pt) {
+    const int64_t p = (int64_t)pt;
+    const int64_t i = p % g.nx;
+    const int64_t j = (p / g.nx) % g.ny;
+    const int64_t k = p / (g.nx * g.ny);
+    x = __dmul_rn((double)i, g.h);
+    y = __dmul_rn((double)j, g.h);
+    const double d = __dmul_rn((double)k, g.h);
+    dd = __dmul_rn(d, d);
+    base = g.base;
+    coef = g.p[0];
+    vk = g.p[1];
+    cap = g.p[2];
+    beam = g.beam_d;
+  }
+
+  __device__ __forceinline__ double temp(int64_t n) const {
+    const double bx = __ldg(beam + 3 * n), by = __ldg(beam + 3 * n + 1),
+                 dir = __ldg(beam + 3 * n + 2);
+    const double xi = __dmul_rn(__dsub_rn(x, bx), dir);
+    const double eta = __dsub_rn(y, by);
+    const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xi, xi), __dmul_rn(eta, eta)), dd));
+    const double arg = __dmul_rn(vk, __dadd_rn(r, xi));  // >= 0
+    double tt;
+    if (arg > 708.0) {
+      tt = base;  // fast_exp == 0 exactly; (coef/r)*0 == +0 (r > 0 here)
+    } else {
+      tt = __dadd_rn(base, __dmul_rn(__ddiv_rn(coef, r), exp_core(-arg)));
+    }
+    return tt > cap ? cap : tt;
+  }
+};
+
+}  // namespace ti64

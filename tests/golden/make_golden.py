@@ -1,0 +1,294 @@
+"""Generate the golden fixtures under tests/golden/ from the REAL reference.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ti64micro from /root/reference/pkg/src (numba, read-only tree;
+NUMBA_CACHE_DIR is pointed at /tmp) and records inputs and outputs of the
+reference's own entry points:
+
+  fastmath.npz   fast_exp / fast_ln / fast_pow on sweeps + special values
+                 (fastmath.py:246-258)
+  steps.npz      step_all cases (batch.py:762): the reference's own test
+                 fixtures (conftest.random_states, bench.generate_layout,
+                 alternating hot/cold, N=13 tail, identical points),
+                 stuck-state seeding sequences, subcycling; every lane width
+  advance_cfg*.npz  multi-step runs where temperature_new is filled each step
+                 from this project's generator definitions (computed by the
+                 oracle's generator) and the kinetics are the
+                 reference's step_all; counters per DESIGN.md §3 in numpy
+  history.npz    integrate_history (integrator.py:303-325)
+  stencil.npz    thermal._stencil_step via step_thermal (thermal.py:321-354)
+
+The GPU box never runs this script (no /root/reference there); tests read
+only the committed .npz files.
+"""
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+REF = Path("/root/reference/pkg")
+OUT = Path(__file__).resolve().parent
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ti64_numba_cache")
+sys.path.insert(0, str(REF / "src"))
+sys.path.insert(0, str(REF / "tests"))
+sys.path.insert(0, str(ROOT))
+
+from ti64micro import fastmath as fm  # noqa: E402
+from ti64micro.batch import GlobalFields, step_all  # noqa: E402
+from ti64micro.bench import generate_layout  # noqa: E402
+from ti64micro.integrator import IntegratorConfig, integrate_history  # noqa: E402
+from ti64micro.kinetics import DEFAULT_PARAMS  # noqa: E402
+from ti64micro import thermal as th  # noqa: E402
+from conftest import random_states  # noqa: E402
+
+from oracle import oracle as orc  # noqa: E402  (generator definitions only)
+from paper_2402_17580_b200 import sources  # noqa: E402
+
+CFG_E = IntegratorConfig(scheme="explicit")
+NAMES = ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old",
+         "temperature_new", "seed_tracked", "seed_active", "seed_direction")
+
+
+def fields_dict(f, prefix):
+    return {f"{prefix}{k}": np.array(getattr(f, k)) for k in NAMES}
+
+
+def make_fastmath():
+    rng = np.random.default_rng(101)
+    special = np.array([0.0, 1.0, -1.0, -1.36, -750.0, 800.0, np.nan, -708.0,
+                        -708.0000001, 709.0, 709.0000001, 1e-300, -1e-300,
+                        -707.9, 708.9, np.inf, -np.inf, 0.5, -0.5, 1e-20])
+    x_exp = np.concatenate([special, np.linspace(-700.0, 709.0, 20001),
+                            rng.uniform(-60, 5, 20000)])
+    special_ln = np.array([1.0, np.e, 2.0, 0.0, -1.0, np.nan, 1e-310, 5e-324,
+                           2.2250738585072014e-308, 1e-300, 1e300, np.inf,
+                           0.9, 1e-14, 0.1, 0.09999999999999998])
+    x_ln = np.concatenate([special_ln,
+                           np.exp(np.linspace(np.log(1e-300), np.log(1e300), 20001)),
+                           1.0 + np.linspace(-1e-3, 1e-3, 2001),
+                           rng.uniform(0, 1, 20000)])
+    a = np.concatenate([[0.25, 0.9, 1.0, -1.0, 1e-300, 0.0],
+                        10.0 ** rng.uniform(-12, 0, 20000)])
+    p = np.concatenate([[0.5, 1.0, 1.398, 2.0, 0.6015936254980079, 1.0],
+                        rng.uniform(0.0, 2.0, 20000)])
+    np.savez_compressed(OUT / "fastmath.npz", x_exp=x_exp, y_exp=fm.fast_exp(x_exp),
+                        x_ln=x_ln, y_ln=fm.fast_ln(x_ln), a_pow=a, x_pow=p,
+                        y_pow=fm.fast_pow(a, p))
+
+
+def seeding_fields():
+    """Stuck compositions and neighbours at temperatures that trigger and end
+    both seeding directions (batch.py:419-464)."""
+    temps = [300.0, 600.0, 847.0, 848.0, 900.0, 934.0, 935.001, 1000.0, 1100.0,
+             1200.0, 1272.0, 1273.5, 1300.0, 1877.0, 1880.0, 1930.0]
+    states = [(0.9, 0.0, 0.1), (0.9, 0.0, 0.09999999999999998), (0.0, 0.0, 1.0),
+              (0.0, 0.0, 0.99), (1e-15, 0.0, 1.0), (0.9 - 5e-15, 0.0, 0.1),
+              (0.9, 1e-15, 0.1), (0.45, 0.0, 0.55), (0.0, 0.3, 0.7)]
+    xs, xm, xb, t0, t1 = [], [], [], [], []
+    for (a, b, c) in states:
+        for ta in temps:
+            for dT in (0.0, 5.0, -5.0):
+                xs.append(a), xm.append(b), xb.append(c)
+                t0.append(ta), t1.append(ta + dT)
+    return GlobalFields(np.array(xs), np.array(xm), np.array(xb), np.array(t0),
+                        np.array(t1))
+
+
+def run_steps(f, dt, lanes, nsteps=1, threads=1, vary=None):
+    for s in range(nsteps):
+        if vary is not None:
+            f.temperature_new[:] = vary(s)
+        step_all(f, dt, DEFAULT_PARAMS, CFG_E, n_lanes=lanes, threads=threads)
+
+
+def make_steps():
+    cases = {}
+
+    def add(name, f, dt, lanes, nsteps=1, threads=1, vary=None):
+        d = fields_dict(f, "in_")
+        g = f.copy()
+        run_steps(g, dt, lanes, nsteps, threads, vary)
+        d.update(fields_dict(g, "out_"))
+        d["dt"] = np.float64(dt)
+        d["lanes"] = np.int64(lanes)
+        d["nsteps"] = np.int64(nsteps)
+        if vary is not None:
+            d["t_seq"] = np.stack([vary(s) for s in range(nsteps)])
+        for k, v in d.items():
+            cases[f"{name}/{k}"] = v
+
+    for lanes in (1, 2, 4, 8):
+        add(f"random257_l{lanes}", random_states(257, seed=3), 2e-5, lanes)
+    add("random4099_thr2", random_states(4099, seed=9), 2e-5, 8, threads=2)
+    add("tail13_l8", random_states(13, seed=6), 2e-5, 8)
+    add("tail13_l1", random_states(13, seed=6), 2e-5, 1)
+    n = 64
+    xs = np.where(np.arange(n) % 2 == 0, 0.2, 0.8)
+    t = np.where(np.arange(n) % 2 == 0, 1000.0, 1150.0)
+    add("alternating_l8", GlobalFields(xs, np.zeros(n), 1.0 - xs, t, t + 1.0), 2e-5, 8)
+    for block in (1, 10, 100):
+        add(f"layout_b{block}", generate_layout(block, 4096, seed=block), 0.01, 8)
+        add(f"layout_b{block}_dt2e-5", generate_layout(block, 4096, seed=block), 2e-5, 8)
+    m = 1000
+    add("identical", GlobalFields(np.full(m, 0.3), np.full(m, 0.1), np.full(m, 0.6),
+                                  np.full(m, 1000.0), np.full(m, 995.0)), 2e-5, 8)
+    add("sub_dt0.05", random_states(32, seed=12, dt_jitter=0.0), 0.05, 8)
+    add("sub_dt0.05_jit", random_states(32, seed=11), 0.05, 8)
+    add("sub_dt0.01", random_states(32, seed=12, dt_jitter=0.0), 0.01, 8)
+    add("sub_dt1.0", random_states(64, seed=15), 1.0, 4)
+    add("hot_liquid", random_states(200, seed=16, t_lo=1800.0, t_hi=3000.0), 1e-4, 8)
+    add("cold", random_states(200, seed=17, t_lo=293.0, t_hi=900.0), 1e-4, 8)
+    for lanes in (1, 8):
+        add(f"seed_1step_l{lanes}", seeding_fields(), 1e-4, lanes)
+        sf = seeding_fields()
+        base_t0 = sf.temperature_old.copy()
+        add(f"seed_40step_l{lanes}", sf, 1e-3, lanes, nsteps=40,
+            vary=lambda s, b=base_t0: b + 3.0 * np.sin(0.3 * s) * (np.arange(len(b)) % 3))
+    np.savez_compressed(OUT / "steps.npz", **cases)
+
+
+def argmax3(xs, xm, xb):
+    return np.where((xs >= xm) & (xs >= xb), 0, np.where(xm >= xb, 1, 2))
+
+
+def make_advance(cfg_id, n, nsteps, snap_every, lanes=8, point_offset=0, src=None,
+                 name=None):
+    """Reference step_all driven by the project's generator."""
+    src = src or sources.source_for_config(cfg_id)
+    beam = src.beam_table(nsteps + 1) if cfg_id == 1 else None
+    gen = src.tempgen(point_offset=point_offset,
+                      beam_ptr=None if beam is None else beam.ctypes.data,
+                      beam_steps=0 if beam is None else len(beam))
+    init = orc.gen_initial_state(gen, n)
+    t0 = orc.gen_temperature(gen, n, 0)
+    f = GlobalFields(init.x_alpha_s, init.x_alpha_m, init.x_beta, t0, t0.copy())
+    kp = DEFAULT_PARAMS.kernel_tuple()
+    mart = np.zeros(n, np.uint32)
+    sw = np.zeros(n, np.uint32)
+    tot = np.zeros(8, np.uint64)
+    sums = []
+    for s in range(nsteps):
+        f.temperature_new[:] = orc.gen_temperature(gen, n, s + 1)
+        xs, xm, xb = f.x_alpha_s.copy(), f.x_alpha_m.copy(), f.x_beta.copy()
+        xa = xs + xm
+        ramp = 1.0 - fm.fast_exp(-kp.k_alpha_eq * (kp.t_as_start - f.temperature_old))
+        xe0 = np.where(f.temperature_old < kp.t_as_end, 0.9,
+                       np.where(f.temperature_old > kp.t_as_start, 0.0, ramp))
+        grow = (xa < xe0) & (xs > 0.0)
+        am = (xm > 0.0) & (xs > 0.0)
+        dis = (xa > xe0) & (xa < 0.9)
+        tot[0] += n
+        tot[1] += int((f.temperature_new < kp.t_am_start).sum())
+        tot[2] += int((grow | am).sum())
+        tot[3] += int(grow.sum())
+        tot[4] += int(am.sum())
+        tot[5] += int(dis.sum())
+        a0 = argmax3(xs, xm, xb)
+        step_all(f, src.dt, DEFAULT_PARAMS, CFG_E, n_lanes=lanes)
+        m = f.x_alpha_m > xm
+        w = argmax3(f.x_alpha_s, f.x_alpha_m, f.x_beta) != a0
+        mart += m.astype(np.uint32)
+        sw += w.astype(np.uint32)
+        tot[6] += int(m.sum())
+        tot[7] += int(w.sum())
+        if (snap_every > 0 and (s + 1) % snap_every == 0) or s + 1 == nsteps:
+            sums.append([f.x_alpha_s.sum(), f.x_alpha_m.sum(), f.x_beta.sum()])
+    out = dict(cfg=np.int64(cfg_id), n=np.int64(n), nsteps=np.int64(nsteps),
+               snap_every=np.int64(snap_every), lanes=np.int64(lanes),
+               point_offset=np.int64(point_offset), martensite=mart, switches=sw,
+               totals=tot, sums=np.array(sums))
+    out.update(fields_dict(f, "out_"))
+    np.savez_compressed(OUT / (name or f"advance_cfg{cfg_id}.npz"), **out)
+
+
+def make_history():
+    rng = np.random.default_rng(33)
+    cases = {}
+    for h in range(6):
+        knots_t = np.concatenate([[0.0], np.sort(rng.uniform(0.1, 6.0, 5))])
+        knots_T = rng.uniform(293.0, 2000.0, 6)
+        times = np.linspace(0.0, knots_t[-1], 1500 if h % 2 == 0 else 150)
+        temps = np.interp(times, knots_t, knots_T)
+        out = integrate_history(times, temps, config=CFG_E)
+        cases[f"h{h}/times"] = times
+        cases[f"h{h}/temps"] = temps
+        cases[f"h{h}/out"] = out
+    times = np.arange(0.0, 10.0 + 1e-9, 1e-3)
+    temps = 1300.0 + (300.0 - 1300.0) * times / 10.0
+    cases["ramp/times"], cases["ramp/temps"] = times, temps
+    cases["ramp/out"] = integrate_history(times, temps, config=CFG_E)
+    np.savez_compressed(OUT / "history.npz", **cases)
+
+
+def make_stencil():
+    cases = {}
+    tp = th.DEFAULT_THERMAL
+    # (a) general: plate + powder + inactive, losses on, source on, Dirichlet
+    geo = th.BuildGeometry(plate_size=(0.6e-3, 0.6e-3, 0.15e-3),
+                           part_size=(0.4e-3, 0.4e-3, 0.1e-3), voxel=0.05e-3)
+    sched = th.BuildSchedule()
+    field, fields = th.allocate_domain(geo, sched)
+    th.activate_layer(field, fields, geo, sched)
+    rng = np.random.default_rng(5)
+    field.temperature_old[:] = 293.0 + rng.uniform(0, 2500.0, field.temperature_old.shape)
+    field.temperature_old[field.state == 0] = 293.0
+    src = th.HeatSource(w_eff=180.0, radius=0.06e-3, h_powder=geo.voxel)
+    cases["general/src"] = field.temperature_old.copy()
+    cases["general/rc_in"] = field.r_c.copy()
+    cases["general/state"] = field.state.copy()
+    cases["general/z_top"] = np.int64(field.z_top)
+    cases["general/h"] = np.float64(field.h)
+    dt = 2e-6
+    beam = (0.3e-3, 0.28e-3, 180.0, True)
+    th.step_thermal(field, dt, tp, src, beam, losses=True, bottom_dirichlet=293.0, nsub=1)
+    cases["general/dst"] = field.temperature_new.copy()
+    cases["general/rc_out"] = field.r_c.copy()
+    cases["general/dt"] = np.float64(dt)
+    cases["general/beam"] = np.array(beam[:3])
+    cases["general/src_peak"] = np.float64(2.0 * 180.0 / (np.pi * src.radius**2 * src.h_powder))
+    cases["general/src_r2inv"] = np.float64(1.0 / src.radius**2)
+    # (b) all built (config-3 shape, reduced): chained steps with a moving source
+    nz, ny, nx = 8, 16, 16
+    h = 20e-6
+    t_old = np.full((nz, ny, nx), 353.0)
+    t_new = t_old.copy()
+    f2 = th.ThermalField(t_old, t_new, np.ones((nz, ny, nx)),
+                         np.full((nz, ny, nx), th.STATE_BUILT, np.uint8), h, nz)
+    src2 = th.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=h)
+    seq = []
+    for k in range(12):
+        bx = 40e-6 + 20e-6 * k
+        by = 150e-6
+        th.step_thermal(f2, 1e-6, tp, src2, (bx, by, 0.35 * 250.0, True), losses=False,
+                        bottom_dirichlet=353.0, nsub=1)
+        seq.append(f2.temperature_new.copy())
+        f2.temperature_old[...] = f2.temperature_new
+    cases["built/seq"] = np.stack(seq)
+    np.savez_compressed(OUT / "stencil.npz", **cases)
+
+
+if __name__ == "__main__":
+    make_fastmath()
+    print("fastmath done")
+    make_steps()
+    print("steps done")
+    make_history()
+    print("history done")
+    make_stencil()
+    print("stencil done")
+    make_advance(0, 4096, 20000, 1000)
+    print("advance cfg0 done")
+    small1 = sources.RosenthalRaster(nx=32, ny=32, nz=4)
+    make_advance(1, 4096, 2000, 500, src=small1, name="advance_cfg1_small.npz")
+    print("advance cfg1 small done")
+    make_advance(2, 512, 50000, 5000, point_offset=12345)
+    print("advance cfg2 done")
+    make_advance(4, 256, 100000, 10000, point_offset=777)
+    print("advance cfg4 done")
