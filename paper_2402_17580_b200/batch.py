@@ -228,7 +228,8 @@ def beam_table(source, rows, device):
     key = (source, rows, str(device))
     t = _beam_cache.get(key)
     if t is None:
-        tab = source.beam_table(rows)
+        packed = getattr(source, "packed_beam", None)
+        tab = packed(rows) if packed is not None else source.beam_table(rows)
         t = None if tab is None else _torch().from_numpy(tab).to(device)
         if len(_beam_cache) > 8:
             _beam_cache.clear()

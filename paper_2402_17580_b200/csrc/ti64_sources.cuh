@@ -84,10 +84,12 @@ struct PulseSet {
     next_event = nxt;
   }
 
-  __device__ __forceinline__ double temp(int64_t n, double t) {
+  __device__ __forceinline__ double temp(int64_t n, double dt) {
     if (n >= next_event || n < 0) rescan(n);
     double s = base;
     unsigned m = live;
+    if (m == 0u) return s;  // every pulse is an exact no-op: T == base
+    const double t = __dmul_rn(step_to_double(n), dt);
     while (m) {
       const int k = __ffs(m) - 1;
       m &= m - 1;
@@ -149,10 +151,19 @@ __device__ __forceinline__ void init_sweep(PulseSet<MAXP>& ps, const ti64_tempge
   ps.live = 0u;
 }
 
-// config 1 (TI64_SRC_ROSENTHAL): p = {coef, v/(2 alpha), cap}
+// config 1 (TI64_SRC_ROSENTHAL): p = {coef, v/(2 alpha), cap, arg_noop_f32,
+// T_noop}.  beam_d holds beam_steps rows of 3 doubles (x, y, dir), padded to
+// an even count, followed by beam_steps rows of 4 floats (x, y, dir, 0) for
+// the FP32 no-op filter (sources.RosenthalRaster.packed_beam).
+//
+// No-op filter: when vk*(R + xi) >= arg_noop the Rosenthal term
+// (coef/R)*fast_exp(-arg) is below a quarter-ulp of `base` (host-derived bound,
+// sources.py), so T == min(base, cap) exactly.  An FP32 estimate of the
+// argument (error < 1e-2 on this lattice) against arg_noop + 1 selects that
+// case without any FP64 work; everything else takes the exact FP64 path.
 struct Rosenthal {
-  double x, y, dd, base, coef, vk, cap;
-  const double* beam;
+  double x, y, dd;
+  float xf, yf, ddf, vkf, thrf;
 
   __device__ __forceinline__ void init(const ti64_tempgen& g, uint64_t pt) {
     const int64_t p = (int64_t)pt;
@@ -163,27 +174,34 @@ struct Rosenthal {
     y = __dmul_rn((double)j, g.h);
     const double d = __dmul_rn((double)k, g.h);
     dd = __dmul_rn(d, d);
-    base = g.base;
-    coef = g.p[0];
-    vk = g.p[1];
-    cap = g.p[2];
-    beam = g.beam_d;
+    xf = (float)x;
+    yf = (float)y;
+    ddf = (float)dd;
+    vkf = (float)g.p[1];
+    thrf = (float)g.p[3];
   }
 
-  __device__ __forceinline__ double temp(int64_t n) const {
-    const double bx = __ldg(beam + 3 * n), by = __ldg(beam + 3 * n + 1),
-                 dir = __ldg(beam + 3 * n + 2);
+  __device__ __forceinline__ double temp(int64_t n, const ti64_tempgen& g) const {
+    const float4 bf = __ldg(
+        reinterpret_cast<const float4*>(g.beam_d + ((3 * g.beam_steps + 1) & ~1LL)) + n);
+    const float xif = (xf - bf.x) * bf.z;
+    const float etaf = yf - bf.y;
+    const float sf = fmaf(xif, xif, fmaf(etaf, etaf, ddf));
+    const float rf = sf * rsqrtf(sf);  // NaN at sf == 0 -> exact path
+    if (vkf * (rf + xif) > thrf) return g.p[4];
+    const double* b = g.beam_d + 3 * n;
+    const double bx = __ldg(b), by = __ldg(b + 1), dir = __ldg(b + 2);
     const double xi = __dmul_rn(__dsub_rn(x, bx), dir);
     const double eta = __dsub_rn(y, by);
     const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xi, xi), __dmul_rn(eta, eta)), dd));
-    const double arg = __dmul_rn(vk, __dadd_rn(r, xi));  // >= 0
+    const double arg = __dmul_rn(g.p[1], __dadd_rn(r, xi));  // >= 0
     double tt;
     if (arg > 708.0) {
-      tt = base;  // fast_exp == 0 exactly; (coef/r)*0 == +0 (r > 0 here)
+      tt = g.base;  // fast_exp == 0 exactly; (coef/r)*0 == +0 (r > 0 here)
     } else {
-      tt = __dadd_rn(base, __dmul_rn(__ddiv_rn(coef, r), exp_core(-arg)));
+      tt = __dadd_rn(g.base, __dmul_rn(__ddiv_rn(g.p[0], r), exp_core(-arg)));
     }
-    return tt > cap ? cap : tt;
+    return tt > g.p[2] ? g.p[2] : tt;
   }
 };
 

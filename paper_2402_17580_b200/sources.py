@@ -113,13 +113,48 @@ class RosenthalRaster:
             out[n, 2] = d
         return out
 
+    def packed_beam(self, n_rows):
+        """Device layout of the beam table: the (n_rows, 3) doubles, padded to
+        an even count, then n_rows float32 rows (x, y, dir, 0) for the kernel's
+        FP32 no-op filter; returned as one float64 array."""
+        tab = self.beam_table(n_rows)
+        nd = 3 * n_rows + (3 * n_rows) % 2
+        out = np.zeros(nd + 2 * n_rows)
+        out[:3 * n_rows] = tab.ravel()
+        f = np.zeros((n_rows, 4), np.float32)
+        f[:, :3] = tab
+        out[nd:] = f.view(np.float64).ravel()
+        return out
+
+    def noop_threshold(self):
+        """(arg_noop_f32, T_noop): for vk*(R+xi) >= arg_noop the source term
+        (coef/R)*fast_exp(-arg) < ulp(base)/4, so T == min(base, cap) bit for
+        bit (R >= arg/(2 vk) bounds coef/R; fast_exp's relative error is
+        < 1e-9).  arg_noop_f32 adds a margin far above the FP32 estimate's
+        error on this lattice."""
+        coef, vk = self._coef_vk()
+        quarter_ulp = math.ulp(self.ambient) / 4.0
+        arg = 1.0
+        while 2.0 * vk * coef / arg * math.exp(-arg) * 1.01 >= quarter_ulp:
+            arg += 1.0
+        extent = math.sqrt((self.nx * self.h) ** 2 + (self.ny * self.h) ** 2 +
+                           (self.nz * self.h) ** 2) + self.track_length + \
+            self.n_tracks * self.hatch
+        margin = max(1.0, 64.0 * vk * 1.2e-7 * extent)
+        return arg + margin, min(self.ambient, self.cap)
+
+    def _coef_vk(self):
+        coef = self.absorptivity * self.power / (2.0 * math.pi * self.conductivity)
+        vk = self.speed / (2.0 * self.diffusivity)
+        return coef, vk
+
     def tempgen(self, point_offset=0, beam_ptr=None, beam_steps=0):
         g = _abi.TempGen()
         g.kind, g.max_pulses, g.seed = self.kind, 0, self.seed
         g.point_offset, g.dt, g.base = point_offset, self.dt, self.ambient
-        coef = self.absorptivity * self.power / (2.0 * math.pi * self.conductivity)
-        vk = self.speed / (2.0 * self.diffusivity)
-        _fill(g, (coef, vk, self.cap))
+        coef, vk = self._coef_vk()
+        thr, t_noop = self.noop_threshold()
+        _fill(g, (coef, vk, self.cap, thr, t_noop))
         g.beam_d = beam_ptr
         g.beam_steps = beam_steps
         g.nx, g.ny, g.nz, g.h = self.nx, self.ny, self.nz, self.h
