@@ -181,15 +181,19 @@ struct Rosenthal {
     thrf = (float)g.p[3];
   }
 
-  __device__ __forceinline__ double temp(int64_t n, const ti64_tempgen& g) const {
-    const float4 bf = __ldg(
-        reinterpret_cast<const float4*>(g.beam_d + ((3 * g.beam_steps + 1) & ~1LL)) + n);
+  static __device__ __forceinline__ const float4* ftab(const ti64_tempgen& g) {
+    return reinterpret_cast<const float4*>(g.beam_d + ((3 * g.beam_steps + 1) & ~1LL));
+  }
+
+  // bfp -> float row of step n, b -> double row of step n
+  __device__ __forceinline__ double temp(const float4* bfp, const double* b,
+                                         const ti64_tempgen& g) const {
+    const float4 bf = __ldg(bfp);
     const float xif = (xf - bf.x) * bf.z;
     const float etaf = yf - bf.y;
     const float sf = fmaf(xif, xif, fmaf(etaf, etaf, ddf));
     const float rf = sf * rsqrtf(sf);  // NaN at sf == 0 -> exact path
     if (vkf * (rf + xif) > thrf) return g.p[4];
-    const double* b = g.beam_d + 3 * n;
     const double bx = __ldg(b), by = __ldg(b + 1), dir = __ldg(b + 2);
     const double xi = __dmul_rn(__dsub_rn(x, bx), dir);
     const double eta = __dsub_rn(y, by);

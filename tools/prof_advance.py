@@ -18,6 +18,7 @@ ap.add_argument("--steps", type=int, default=1000)
 ap.add_argument("--step0", type=int, default=0)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--pre", type=int, default=0, help="untimed steps before the measured launches")
 a = ap.parse_args()
 src = pkg.source_for_config(a.config)
 n = a.n or (src.n_points if a.config == 1 else {0: 4096, 2: 1 << 24, 4: 1 << 24}[a.config])
@@ -25,6 +26,9 @@ f0 = pkg.init_from_source(src, n)
 if a.step0:
     from paper_2402_17580_b200.batch import gen_temperature
     f0.temperature_old.copy_(gen_temperature(src, n, a.step0))
+if a.pre:
+    pkg.advance(f0, a.pre, src, step0=a.step0)
+    a.step0 += a.pre
 for r in range(a.reps):
     f = f0.copy()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
