@@ -62,7 +62,7 @@ class TempGen(C.Structure):
                 ("dt", C.c_double), ("base", C.c_double),
                 ("p", C.c_double * 16), ("beam_d", C.c_void_p),
                 ("beam_steps", C.c_int64), ("nx", C.c_int64), ("ny", C.c_int64),
-                ("nz", C.c_int64), ("h", C.c_double)]
+                ("nz", C.c_int64), ("h", C.c_double), ("pf", C.c_float * 8)]
 
 
 class Counters(C.Structure):

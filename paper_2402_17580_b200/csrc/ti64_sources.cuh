@@ -31,6 +31,18 @@ __device__ __forceinline__ double unif(double lo, double hi, double u) {
   return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u));
 }
 
+// single-MUFU FP32 approximations (used only for conservative estimates)
+__device__ __forceinline__ float exp2f_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrtf_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // (double)n exactly, n in [0, 2^52): one DADD instead of an I2F conversion
 __device__ __forceinline__ double step_to_double(int64_t n) {
   return __dsub_rn(__hiloint2double(0x43300000 | (int)(n >> 32), (int)(uint32_t)n),
@@ -82,6 +94,23 @@ struct PulseSet {
       }
     }
     next_event = nxt;
+  }
+
+  // FP32 estimate of T - base (relative error < 1e-5; u is formed in FP64
+  // so the only FP32 error is in the exponential and the product).
+  __device__ __forceinline__ float excess_estimate(int64_t n, double dt) {
+    if (n >= next_event || n < 0) rescan(n);
+    unsigned m = live;
+    if (m == 0u) return 0.0f;
+    const double t = __dmul_rn(step_to_double(n), dt);
+    float e = 0.0f;
+    while (m) {
+      const int k = __ffs(m) - 1;
+      m &= m - 1;
+      const float u = (float)__dmul_rn(__dsub_rn(t, tc[k]), inv_w[k]);
+      e += (float)a[k] * exp2f_approx(-u * u * 1.44269504f);
+    }
+    return e;
   }
 
   __device__ __forceinline__ double temp(int64_t n, double dt) {
@@ -163,7 +192,7 @@ __device__ __forceinline__ void init_sweep(PulseSet<MAXP>& ps, const ti64_tempge
 // case without any FP64 work; everything else takes the exact FP64 path.
 struct Rosenthal {
   double x, y, dd;
-  float xf, yf, ddf, vkf, thrf;
+  float xf, yf, ddf;
 
   __device__ __forceinline__ void init(const ti64_tempgen& g, uint64_t pt) {
     const int64_t p = (int64_t)pt;
@@ -177,23 +206,42 @@ struct Rosenthal {
     xf = (float)x;
     yf = (float)y;
     ddf = (float)dd;
-    vkf = (float)g.p[1];
-    thrf = (float)g.p[3];
   }
 
   static __device__ __forceinline__ const float4* ftab(const ti64_tempgen& g) {
     return reinterpret_cast<const float4*>(g.beam_d + ((3 * g.beam_steps + 1) & ~1LL));
   }
 
-  // bfp -> float row of step n, b -> double row of step n
+  // FP32 geometry of step row bf: returns s = R^2 and sets xi
+  __device__ __forceinline__ float geom(const float4& bf, float& xif) const {
+    xif = (xf - bf.x) * bf.z;
+    const float etaf = yf - bf.y;
+    return fmaf(xif, xif, fmaf(etaf, etaf, ddf));
+  }
+
+  // FP32 estimate of T - base (pf = {vk, coef, vk*log2e, ...}); relative
+  // error ~1e-4 on this lattice (coordinates carry 1e-9 m error), NaN when
+  // the point sits on the beam (caller then takes the exact path).
+  __device__ __forceinline__ float excess_estimate(const float4* bfp, const ti64_tempgen& g) const {
+    const float4 bf = __ldg(bfp);
+    float xif;
+    const float sf = geom(bf, xif);
+    const float rq = rsqrtf_approx(sf);
+    const float rf = sf * rq;
+    return g.pf[1] * rq * exp2f_approx(-g.pf[2] * (rf + xif));
+  }
+
+  // exact T at the step rows (bfp float row, b double row)
   __device__ __forceinline__ double temp(const float4* bfp, const double* b,
                                          const ti64_tempgen& g) const {
-    const float4 bf = __ldg(bfp);
-    const float xif = (xf - bf.x) * bf.z;
-    const float etaf = yf - bf.y;
-    const float sf = fmaf(xif, xif, fmaf(etaf, etaf, ddf));
-    const float rf = sf * rsqrtf(sf);  // NaN at sf == 0 -> exact path
-    if (vkf * (rf + xif) > thrf) return g.p[4];
+    {
+      // no-op filter: vk (R + xi) > arg_noop  <=>  R > c := arg_noop/vk - xi
+      const float4 bf = __ldg(bfp);
+      float xif;
+      const float sf = geom(bf, xif);
+      const float c = g.pf[3] - xif;
+      if (c <= 0.0f || sf > c * c) return g.p[4];
+    }
     const double bx = __ldg(b), by = __ldg(b + 1), dir = __ldg(b + 2);
     const double xi = __dmul_rn(__dsub_rn(x, bx), dir);
     const double eta = __dsub_rn(y, by);

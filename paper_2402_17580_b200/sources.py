@@ -158,6 +158,12 @@ class RosenthalRaster:
         g.beam_d = beam_ptr
         g.beam_steps = beam_steps
         g.nx, g.ny, g.nz, g.h = self.nx, self.ny, self.nz, self.h
+        # FP32 constants of the kernel's estimates: vk, coef, vk*log2(e),
+        # arg_noop/vk (the no-op filter compares R against arg_noop/vk - xi)
+        g.pf[0] = vk
+        g.pf[1] = coef
+        g.pf[2] = vk * 1.4426950408889634
+        g.pf[3] = thr / vk
         return g
 
 

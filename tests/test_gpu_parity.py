@@ -161,6 +161,11 @@ def _advance_vs_golden(pkg, fname, src):
     assert np.array_equal(cnt.switches.cpu().numpy().astype(np.uint32), g["switches"])
     assert np.array_equal(cnt.totals.cpu().numpy().astype(np.uint64), g["totals"])
     np.testing.assert_allclose(r.sums.cpu().numpy(), g["sums"], rtol=1e-12, atol=1e-12)
+    # the uncounted kernel (the timed one: range rest + steady skip) too
+    f2 = pkg.init_from_source(src, n, point_offset=int(g["point_offset"]))
+    pkg.advance(f2, nsteps, src, snapshot_every=int(g["snap_every"]),
+                n_lanes=int(g["lanes"]), point_offset=int(g["point_offset"]))
+    assert_fields(f2, {k: g["out_" + k] for k in FIELD_NAMES}, fname + " (uncounted)")
 
 
 def test_advance_cfg0_golden(pkg):
