@@ -697,17 +697,22 @@ int64_t oracle_history(const double* times, const double* temps, int64_t ns,
 #define STATE_INACTIVE 0
 #define STATE_POWDER 1
 
+/* Arrays hold global planes [z_base, z_base + nz_stored) (the whole grid
+ * when z_base = 0, nz_stored = nz); planes [z_begin, z_end) are updated.
+ * The slab form exists so tests can check the z-slab decomposition of the
+ * multi-GPU driver against the whole-grid reference. */
 void oracle_stencil_step(const double* src, double* dst, double* rc,
                          const uint8_t* state, const ti64_thermal* tp,
                          const ti64_stencil_args* a) {
   const int64_t nz = a->nz, ny = a->ny, nx = a->nx;
-#define IDX(z, y, x) (((z) * ny + (y)) * nx + (x))
+  const int64_t zb = a->z_base;
+#define IDX(z, y, x) ((((z) - zb) * ny + (y)) * nx + (x))
   double inv_rch2 = a->dt / (tp->rho_c * a->h * a->h);
   double inv_rch = a->dt / (tp->rho_c * a->h);
   double inv_rc = a->dt / tp->rho_c;
   double dk = tp->k_ms - tp->k_p;
   double t4inf = pow(tp->t_inf, 4.0);
-  for (int64_t z = 0; z < a->z_top; ++z)
+  for (int64_t z = a->z_begin; z < a->z_end; ++z)
     for (int64_t y = 0; y < ny; ++y)
       for (int64_t x = 0; x < nx; ++x) {
         if (state[IDX(z, y, x)] == STATE_INACTIVE) continue;
@@ -760,11 +765,11 @@ void oracle_stencil_step(const double* src, double* dst, double* rc,
         }
         dst[IDX(z, y, x)] = t_new;
       }
-  if (a->bc_bottom_on != 0)
+  if (a->bc_bottom_on != 0 && a->z_begin == 0 && a->z_end > 0)
     for (int64_t y = 0; y < ny; ++y)
       for (int64_t x = 0; x < nx; ++x)
         if (state[IDX(0, y, x)] != STATE_INACTIVE) dst[IDX(0, y, x)] = a->bc_bottom;
-  for (int64_t z = 0; z < a->z_top; ++z)
+  for (int64_t z = a->z_begin; z < a->z_end; ++z)
     for (int64_t y = 0; y < ny; ++y)
       for (int64_t x = 0; x < nx; ++x)
         if (state[IDX(z, y, x)] == STATE_POWDER) {

@@ -86,7 +86,31 @@ class StencilArgs(C.Structure):
                 ("source_on", C.c_int32), ("losses_on", C.c_int32),
                 ("bc_bottom_on", C.c_int32), ("all_built", C.c_int32),
                 ("src_peak", C.c_double), ("src_r2inv", C.c_double),
-                ("bc_bottom", C.c_double)]
+                ("bc_bottom", C.c_double), ("z_base", C.c_int64),
+                ("nz_stored", C.c_int64), ("z_begin", C.c_int64), ("z_end", C.c_int64)]
+
+
+def stencil_args(nx, ny, nz, z_top, dt, h, beam=None, source=None, losses=False,
+                 bottom=None, all_built=False, slab=None):
+    """StencilArgs for a whole grid (slab=None) or a z-slab
+    slab=(z_base, nz_stored, z_begin, z_end)."""
+    import math
+    a = StencilArgs(nx=nx, ny=ny, nz=nz, z_top=z_top, dt=dt, h=h)
+    if beam is not None and source is not None and beam[3]:
+        a.beam_x, a.beam_y = beam[0], beam[1]
+        a.src_peak = 2.0 * beam[2] / (math.pi * source.radius ** 2 * source.h_powder)
+        a.src_r2inv = 1.0 / source.radius ** 2
+        a.source_on = 1
+    else:
+        a.src_r2inv = 1.0
+    a.losses_on = 1 if losses else 0
+    a.bc_bottom_on = 0 if bottom is None else 1
+    a.bc_bottom = 0.0 if bottom is None else float(bottom)
+    a.all_built = 1 if all_built else 0
+    if slab is None:
+        slab = (0, nz, 0, z_top)
+    a.z_base, a.nz_stored, a.z_begin, a.z_end = slab
+    return a
 
 
 def kparams_from(kernel_tuple):

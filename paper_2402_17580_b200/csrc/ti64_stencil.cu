@@ -54,6 +54,9 @@ __device__ __forceinline__ double add_source(double t_new, int64_t x, int64_t y,
 
 constexpr int TX = 32, TY = 8;
 
+// Arrays hold global planes [z_base, z_base + nz_stored); the block updates
+// global planes [z0, z1) of its z-chunk.  z-1 / z / z+1 ride in registers, the
+// current plane (+ x/y halo) is staged in shared memory.
 __global__ void __launch_bounds__(TX* TY) stencil_built_kernel(const double* __restrict__ src,
                                                              double* __restrict__ dst,
                                                              ti64_stencil_args a,
@@ -63,27 +66,28 @@ __global__ void __launch_bounds__(TX* TY) stencil_built_kernel(const double* __r
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t x = (int64_t)blockIdx.x * TX + tx;
   const int64_t y = (int64_t)blockIdx.y * TY + ty;
-  const int64_t z0 = (int64_t)blockIdx.z * zchunk;
+  const int64_t z0 = a.z_begin + (int64_t)blockIdx.z * zchunk;
   int64_t z1 = z0 + zchunk;
-  if (z1 > a.z_top) z1 = a.z_top;
+  if (z1 > a.z_end) z1 = a.z_end;
   const bool in = x < nx && y < ny;
   const int64_t plane = nx * ny;
   const int64_t col = y * nx + x;
+  const double* sp = src + (-a.z_base) * plane + col;  // sp[z*plane] = T(z, y, x)
+  double* dp = dst + (-a.z_base) * plane + col;
   const double kf = c.kf;
   double tm = 0.0, t0 = 0.0, tp = 0.0;
   if (in && z0 < z1) {
-    t0 = src[z0 * plane + col];
-    if (z0 > 0) tm = src[(z0 - 1) * plane + col];
+    t0 = sp[z0 * plane];
+    if (z0 > 0) tm = sp[(z0 - 1) * plane];
   }
   for (int64_t z = z0; z < z1; ++z) {
-    if (in && z + 1 < nz) tp = src[(z + 1) * plane + col];
-    // stage the plane with a 1-cell x/y halo
+    if (in && z + 1 < nz) tp = sp[(z + 1) * plane];
     __syncthreads();
     if (in) pl[ty + 1][tx + 1] = t0;
-    if (tx == 0 && x > 0 && y < ny) pl[ty + 1][0] = src[z * plane + col - 1];
-    if (tx == TX - 1 && x + 1 < nx && y < ny) pl[ty + 1][TX + 1] = src[z * plane + col + 1];
-    if (ty == 0 && y > 0 && x < nx) pl[0][tx + 1] = src[z * plane + col - nx];
-    if (ty == TY - 1 && y + 1 < ny && x < nx) pl[TY + 1][tx + 1] = src[z * plane + col + nx];
+    if (tx == 0 && x > 0 && y < ny) pl[ty + 1][0] = sp[z * plane - 1];
+    if (tx == TX - 1 && x + 1 < nx && y < ny) pl[ty + 1][TX + 1] = sp[z * plane + 1];
+    if (ty == 0 && y > 0 && x < nx) pl[0][tx + 1] = sp[z * plane - nx];
+    if (ty == TY - 1 && y + 1 < ny && x < nx) pl[TY + 1][tx + 1] = sp[z * plane + nx];
     __syncthreads();
     if (in) {
       double flux = 0.0;
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(TX* TY) stencil_built_kernel(const double* __r
       double t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
       if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
       if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
-      dst[z * plane + col] = t_new;
+      dp[z * plane] = t_new;
     }
     tm = t0;
     t0 = tp;
@@ -112,9 +116,10 @@ __global__ void __launch_bounds__(256) stencil_general_kernel(const double* __re
                                                              StencilConst c) {
   const int64_t nx = a.nx, ny = a.ny, nz = a.nz;
   const int64_t plane = nx * ny;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= a.z_top * plane) return;
-  const int64_t z = idx / plane, y = (idx / nx) % ny, x = idx % nx;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (a.z_end - a.z_begin) * plane) return;
+  const int64_t z = a.z_begin + t / plane, y = (t / nx) % ny, x = t % nx;
+  const int64_t idx = (z - a.z_base) * plane + y * nx + x;  // stored index
   if (state[idx] == STATE_INACTIVE) return;
   const double t0 = src[idx];
   const double g0 = clip01(__ddiv_rn(__dsub_rn(t0, tp.t_sol), c.dliq));
@@ -132,7 +137,7 @@ __global__ void __launch_bounds__(256) stencil_general_kernel(const double* __re
     else if (face == 4) zz = z - 1;
     else zz = z + 1;
     if (xx < 0 || xx >= nx || yy < 0 || yy >= ny || zz < 0 || zz >= nz) continue;
-    const int64_t j = (zz * ny + yy) * nx + xx;
+    const int64_t j = ((zz - a.z_base) * ny + yy) * nx + xx;
     if (state[j] == STATE_INACTIVE) continue;
     const double t1 = src[j];
     const double g1 = clip01(__ddiv_rn(__dsub_rn(t1, tp.t_sol), c.dliq));
@@ -167,10 +172,10 @@ __global__ void __launch_bounds__(256) stencil_general_kernel(const double* __re
 
 // running max consolidation of powder cells on the post-step field
 __global__ void consolidate_kernel(const double* __restrict__ dst, double* __restrict__ rc,
-                                   const uint8_t* __restrict__ state, int64_t n, double t_sol,
-                                   double dliq) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || state[i] != STATE_POWDER) return;
+                                   const uint8_t* __restrict__ state, int64_t off, int64_t n,
+                                   double t_sol, double dliq) {
+  const int64_t i = off + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= off + n || state[i] != STATE_POWDER) return;
   const double g1 = clip01(__ddiv_rn(__dsub_rn(dst[i], t_sol), dliq));
   if (g1 > rc[i]) rc[i] = g1;
 }
@@ -183,7 +188,10 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
                                      const uint8_t* state_d, const ti64_thermal* tp,
                                      const ti64_stencil_args* a, void* stream) {
   if (!src_d || !dst_d || !tp || !a || a->nx < 1 || a->ny < 1 || a->nz < 1 || a->z_top < 0 ||
-      a->z_top > a->nz || src_d == dst_d) {
+      a->z_top > a->nz || src_d == dst_d || a->z_begin < 0 || a->z_end > a->z_top ||
+      a->z_begin < a->z_base || a->z_end > a->z_base + a->nz_stored ||
+      (a->z_begin > 0 && a->z_begin - 1 < a->z_base) ||
+      (a->z_end < a->nz && a->z_end + 1 > a->z_base + a->nz_stored)) {
     ti64_set_error("ti64_stencil_step: bad argument");
     return TI64_EINVAL;
   }
@@ -203,18 +211,20 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
   c.kf = 2.0 * kb * kb / (kb + kb);
   c.dliq = tp->t_liq - tp->t_sol;
   c.src_coef = c.inv_rc * a->src_peak;
-  if (a->z_top == 0) return TI64_OK;
+  const int64_t nzu = a->z_end - a->z_begin;
+  if (nzu <= 0) return TI64_OK;
   if (a->all_built) {
-    const int zchunk = 32;
+    const int zchunk = 16;
     dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TY - 1) / TY),
-              (unsigned)((a->z_top + zchunk - 1) / zchunk));
+              (unsigned)((nzu + zchunk - 1) / zchunk));
     stencil_built_kernel<<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk);
   } else {
-    const int64_t n = a->z_top * a->nx * a->ny;
+    const int64_t plane = a->nx * a->ny;
+    const int64_t n = nzu * plane;
     stencil_general_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src_d, dst_d, rc_d,
                                                                        state_d, *tp, *a, c);
-    consolidate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dst_d, rc_d, state_d, n,
-                                                                    tp->t_sol, c.dliq);
+    consolidate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        dst_d, rc_d, state_d, (a->z_begin - a->z_base) * plane, n, tp->t_sol, c.dliq);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

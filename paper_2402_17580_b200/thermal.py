@@ -100,3 +100,116 @@ class HeatSource:
 def stable_dt(h, params=DEFAULT_THERMAL):
     """Explicit diffusion bound h^2 rho c / (6 k_max) (thermal.py:168-170)."""
     return h * h * params.rho * params.c / (6.0 * params.k_ms)
+
+
+# --------------------------------------------------------------------------
+# device-resident field and the K4 step (thermal.py:177-202, :321-354)
+# --------------------------------------------------------------------------
+
+class ThermalField:
+    """Voxel grid on the GPU (thermal.py:177-202).  temperature_old/new are
+    (nz, ny, nx) views of the kinetics GlobalFields' temperature buffers, so
+    the thermal -> kinetics hand-off is the in-place roll of step_all, as in
+    the reference (thermal.py:424-431)."""
+
+    def __init__(self, temperature_old, temperature_new, r_c, state, h, z_top):
+        self.temperature_old = temperature_old
+        self.temperature_new = temperature_new
+        self.r_c = r_c
+        self.state = state
+        self.h = float(h)
+        self.z_top = int(z_top)
+
+    @property
+    def shape(self):
+        return tuple(self.state.shape)
+
+    def all_built(self):
+        """True when every cell is STATE_BUILT with r_c == 1 (config 3)."""
+        return bool((self.state == STATE_BUILT).all().item() and
+                    (self.r_c == 1.0).all().item())
+
+
+def step_thermal(field, dt, params=DEFAULT_THERMAL, source=None, beam=None, losses=True,
+                 bottom_dirichlet=None, nsub=None, all_built=None, stream=None):
+    """Advance the thermal field by dt (thermal.py:321-354) with K4.
+
+    temperature_old is left untouched and temperature_new receives the
+    result; nsub > 1 alternates through scratch buffers exactly as
+    _thermal_substeps (thermal.py:290-318).  Raises ValueError when a forced
+    substep count violates the stability bound.
+    """
+    import ctypes as C
+    import torch
+    from . import _abi, _lib
+    lib = _lib.require()
+    dt_ok = stable_dt(field.h, params)
+    if nsub is None:
+        nsub = max(1, int(math.ceil(dt / dt_ok - 1e-12)))
+    if dt / nsub > dt_ok * (1 + 1e-9):
+        raise ValueError(f"dt/nsub={dt/nsub:.3e} exceeds stability bound {dt_ok:.3e} s")
+    nz, ny, nx = field.shape
+    if all_built is None:
+        all_built = field.all_built()
+    a = _abi.stencil_args(nx, ny, nz, field.z_top, dt / nsub, field.h, beam=beam,
+                          source=source, losses=losses, bottom=bottom_dirichlet,
+                          all_built=all_built)
+    tp = _abi.thermal_from(params.kernel_tuple())
+    st = _lib.stream_handle(stream)
+    cur = field.temperature_old
+    bufs = [None, None]
+    for s in range(nsub):
+        if s == nsub - 1:
+            dst = field.temperature_new
+        else:
+            if bufs[s % 2] is None:
+                bufs[s % 2] = torch.empty_like(field.temperature_old)
+            dst = bufs[s % 2]
+        rc = lib.ti64_stencil_step(_lib.ptr(cur), _lib.ptr(dst), _lib.ptr(field.r_c),
+                                   _lib.ptr(field.state), C.byref(tp), C.byref(a), st)
+        _lib.check(rc, "ti64_stencil_step")
+        cur = dst
+    return field
+
+
+class CoupledDomain:
+    """Config 3: a fully built (nz, ny, nx) block, kinetics state at every
+    cell, driven per step exactly as run_build's `couple` does
+    (thermal.py:541-555): step_thermal(dt) then step_all(dt) on the aliased
+    temperature buffers."""
+
+    def __init__(self, nx=512, ny=512, nz=256, h=20e-6, t0=353.0, state0=(0.9, 0.0, 0.1),
+                 device=None):
+        import numpy as np
+        import torch
+        from .batch import GlobalFields
+        n = nx * ny * nz
+        t = torch.full((n,), float(t0), dtype=torch.float64)
+        self.fields = GlobalFields(torch.full((n,), float(state0[0]), dtype=torch.float64),
+                                   torch.full((n,), float(state0[1]), dtype=torch.float64),
+                                   torch.full((n,), float(state0[2]), dtype=torch.float64),
+                                   t, t.clone(), device=device)
+        dev = self.fields.device
+        self.field = ThermalField(self.fields.temperature_old.view(nz, ny, nx),
+                                  self.fields.temperature_new.view(nz, ny, nx),
+                                  torch.ones((nz, ny, nx), dtype=torch.float64, device=dev),
+                                  torch.full((nz, ny, nx), STATE_BUILT, dtype=torch.uint8,
+                                             device=dev), h, nz)
+        self.shape = (nz, ny, nx)
+        self.step = 0
+        del np
+
+    def run(self, n_steps, dt, beams, source, kinetics_params=None, integrator_config=None,
+            thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8):
+        """n_steps coupled steps; beams[k] = (x, y, power, on) of step k."""
+        from .batch import step_all
+        from .integrator import IntegratorConfig
+        from .kinetics import DEFAULT_PARAMS
+        kp = kinetics_params or DEFAULT_PARAMS
+        cfg = integrator_config or IntegratorConfig(scheme="explicit")
+        for k in range(n_steps):
+            step_thermal(self.field, dt, thermal_params, source, beams[k], losses=losses,
+                         bottom_dirichlet=bottom, all_built=True)
+            step_all(self.fields, dt, kp, cfg, n_lanes=n_lanes)
+            self.step += 1
+        return self

@@ -88,7 +88,8 @@ def test_stencil_general_bitwise():
                          h=float(c["h"]), beam_x=float(c["beam"][0]),
                          beam_y=float(c["beam"][1]), source_on=1, losses_on=1,
                          bc_bottom_on=1, all_built=0, src_peak=float(c["src_peak"]),
-                         src_r2inv=float(c["src_r2inv"]), bc_bottom=293.0)
+                         src_r2inv=float(c["src_r2inv"]), bc_bottom=293.0,
+                         z_base=0, nz_stored=nz, z_begin=0, z_end=int(c["z_top"]))
     dst = c["src"].copy()
     rc = c["rc_in"].copy()
     orc.stencil_step(c["src"].copy(), dst, rc, c["state"].copy(),
@@ -109,11 +110,9 @@ def test_stencil_built_sequence_bitwise():
     rc = np.ones_like(t)
     state = np.full(t.shape, 2, np.uint8)
     for k in range(seq.shape[0]):
-        a = _abi.StencilArgs(nx=nx, ny=ny, nz=nz, z_top=nz, dt=1e-6, h=h,
-                             beam_x=40e-6 + 20e-6 * k, beam_y=150e-6, source_on=1,
-                             losses_on=0, bc_bottom_on=1, all_built=1,
-                             src_peak=src.peak, src_r2inv=1.0 / src.radius**2,
-                             bc_bottom=353.0)
+        a = _abi.stencil_args(nx, ny, nz, nz, 1e-6, h,
+                              beam=(40e-6 + 20e-6 * k, 150e-6, 0.35 * 250.0, True),
+                              source=src, losses=False, bottom=353.0, all_built=True)
         dst = t.copy()
         orc.stencil_step(t, dst, rc, state, DEFAULT_THERMAL.kernel_tuple(), a)
         assert_bitwise(dst, seq[k], f"built step {k}")
