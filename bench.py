@@ -161,7 +161,7 @@ def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    base = cpu_reference(budget_s=max(2.0, 2.0 * args.steps))
+    base = cpu_reference(budget_s=max(2.0, min(30.0, 1.5 * args.steps)))
     line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
