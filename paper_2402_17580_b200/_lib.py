@@ -10,7 +10,11 @@ from pathlib import Path
 
 from . import _abi
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libti64b200.so"
+import os
+
+# TI64_LIB overrides the in-tree library (kernel-variant experiments only)
+LIB_PATH = Path(os.environ.get("TI64_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libti64b200.so")
 
 __all__ = ["Ti64Unavailable", "Ti64Error", "load", "require", "check", "LIB_PATH"]
 

@@ -16,13 +16,19 @@ import paper_2402_17580_b200 as pkg  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="0,1,2,4")
 ap.add_argument("--window", type=int, default=0, help="steps per config (0 = preset)")
+ap.add_argument("--full", action="store_true", help="the config's whole step count")
+ap.add_argument("--n", type=int, default=0)
 a = ap.parse_args()
 preset = {0: (4096, 20000, 0), 1: (1 << 20, 10000, 0), 2: (1 << 24, 5000, 0),
           4: (1 << 24, 5000, 0)}
 for c in [int(x) for x in a.configs.split(",")]:
     n, steps, step0 = preset[c]
+    if a.n:
+        n = a.n
     if a.window:
         steps = a.window
+    if a.full:
+        steps = {0: 20000, 1: 10000, 2: 50000, 4: 100000}[c] - 200
     src = pkg.source_for_config(c)
     f = pkg.init_from_source(src, n)
     # warm (first 200 steps), then time the window
