@@ -293,7 +293,7 @@ def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
     fields.traffic_bytes += BYTES_PER_POINT * n * n_steps
     fields.steps_taken += n_steps
     return AdvanceResult(sums=sums[:n_snap], counters=counters, steps=n_steps,
-                         launches=2 * n_snap)
+                         launches=3 * n_snap)
 
 
 def init_from_source(source, n, point_offset=0, device=None):
