@@ -280,6 +280,7 @@ def run_b200(args):
 
     # e2e through the public API: pinned host inputs -> H2D, advance, D2H states
     host = {k: torch.from_numpy(pristine.host(k)).pin_memory() for k in pkg.batch.NAMES}
+    out_host = torch.empty((n, 3), dtype=torch.float64).pin_memory()
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     e2e_times = []
     for _ in range(max(1, min(args.steps, 3))):
@@ -287,7 +288,7 @@ def run_b200(args):
         t0 = time.perf_counter()
         f = pkg.GlobalFields(*[host[k] for k in pkg.batch.NAMES], device=dev)
         pkg.advance(f, nsteps, src, snapshot_every=SNAP_EVERY, scratch=scratch)
-        st = f.states()
+        st = f.states(out=out_host)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
     d2h = st.nbytes

@@ -120,10 +120,17 @@ class GlobalFields:
         t = np.full(n, float(temperature))
         return cls(np.zeros(n), np.zeros(n), np.zeros(n), t, t.copy(), device=device)
 
-    def states(self):
-        """(n, 3) numpy array of phase fractions (copied from the device)."""
+    def states(self, out=None):
+        """(n, 3) numpy array of phase fractions (copied from the device).
+
+        `out`: optional (n, 3) float64 host tensor (pin it for full D2H
+        bandwidth) that receives the copy; its numpy view is returned."""
         torch = _torch()
-        return torch.stack([self.x_alpha_s, self.x_alpha_m, self.x_beta], 1).cpu().numpy()
+        st = torch.stack([self.x_alpha_s, self.x_alpha_m, self.x_beta], 1)
+        if out is None:
+            return st.cpu().numpy()
+        out.copy_(st)
+        return out.numpy()
 
     def host(self, name):
         return getattr(self, name).cpu().numpy()
