@@ -23,6 +23,7 @@
 
 #include "../../include/ti64_b200.h"
 #include "ti64_fastmath.cuh"
+#include "ti64_point.cuh"
 
 using namespace ti64;
 
@@ -53,59 +54,6 @@ __device__ __forceinline__ double add_source(double t_new, int64_t x, int64_t y,
 }
 
 constexpr int TX = 32, TY = 8;
-
-// Arrays hold global planes [z_base, z_base + nz_stored); the block updates
-// global planes [z0, z1) of its z-chunk.  z-1 / z / z+1 ride in registers, the
-// current plane (+ x/y halo) is staged in shared memory.
-__global__ void __launch_bounds__(TX* TY) stencil_built_kernel(const double* __restrict__ src,
-                                                             double* __restrict__ dst,
-                                                             ti64_stencil_args a,
-                                                             StencilConst c, int zchunk) {
-  __shared__ double pl[TY + 2][TX + 2];
-  const int64_t nx = a.nx, ny = a.ny, nz = a.nz;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t x = (int64_t)blockIdx.x * TX + tx;
-  const int64_t y = (int64_t)blockIdx.y * TY + ty;
-  const int64_t z0 = a.z_begin + (int64_t)blockIdx.z * zchunk;
-  int64_t z1 = z0 + zchunk;
-  if (z1 > a.z_end) z1 = a.z_end;
-  const bool in = x < nx && y < ny;
-  const int64_t plane = nx * ny;
-  const int64_t col = y * nx + x;
-  const double* sp = src + (-a.z_base) * plane + col;  // sp[z*plane] = T(z, y, x)
-  double* dp = dst + (-a.z_base) * plane + col;
-  const double kf = c.kf;
-  double tm = 0.0, t0 = 0.0, tp = 0.0;
-  if (in && z0 < z1) {
-    t0 = sp[z0 * plane];
-    if (z0 > 0) tm = sp[(z0 - 1) * plane];
-  }
-  for (int64_t z = z0; z < z1; ++z) {
-    if (in && z + 1 < nz) tp = sp[(z + 1) * plane];
-    __syncthreads();
-    if (in) pl[ty + 1][tx + 1] = t0;
-    if (tx == 0 && x > 0 && y < ny) pl[ty + 1][0] = sp[z * plane - 1];
-    if (tx == TX - 1 && x + 1 < nx && y < ny) pl[ty + 1][TX + 1] = sp[z * plane + 1];
-    if (ty == 0 && y > 0 && x < nx) pl[0][tx + 1] = sp[z * plane - nx];
-    if (ty == TY - 1 && y + 1 < ny && x < nx) pl[TY + 1][tx + 1] = sp[z * plane + nx];
-    __syncthreads();
-    if (in) {
-      double flux = 0.0;
-      if (x > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(pl[ty + 1][tx], t0)));
-      if (x + 1 < nx) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(pl[ty + 1][tx + 2], t0)));
-      if (y > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(pl[ty][tx + 1], t0)));
-      if (y + 1 < ny) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(pl[ty + 2][tx + 1], t0)));
-      if (z > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(tm, t0)));
-      if (z + 1 < nz) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(tp, t0)));
-      double t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
-      if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
-      if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
-      dp[z * plane] = t_new;
-    }
-    tm = t0;
-    t0 = tp;
-  }
-}
 
 __global__ void __launch_bounds__(256) stencil_general_kernel(const double* __restrict__ src,
                                                              double* __restrict__ dst,
@@ -180,6 +128,174 @@ __global__ void consolidate_kernel(const double* __restrict__ dst, double* __res
   if (g1 > rc[i]) rc[i] = g1;
 }
 
+// ---------------------------------------------------------------------------
+// Fused coupled step (config 3): K4 built stencil + the kinetics step per cell
+// ---------------------------------------------------------------------------
+constexpr double IDLE_XB = 1.0 - 0.9;
+
+__device__ __forceinline__ bool bits_same(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// cold idle composition (0.9, +0, 1 - 0.9) with the seed inactive
+__device__ __forceinline__ bool idle_cell(double xs, double xm, double xb, int ac) {
+  return ac == 0 && bits_same(xs, 0.9) && __double_as_longlong(xm) == 0 && bits_same(xb, IDLE_XB);
+}
+
+struct CoupledODE {
+  ti64_kparams kp;
+  Derived dv;
+  ti64_icfg cfg;
+  double dt;
+  int L;
+  int rest_ok;  // t_as_end <= t_sol etc.: the cold idle rest is exact
+};
+
+// ---------------------------------------------------------------------------
+// Pipelined z-marching kernel for all-built grids (K4), optionally fused with
+// the kinetics step of every cell (config 3).
+//
+// A block owns a TX x TY (x, y) tile and a z-range.  Planes (+1-cell x/y halo)
+// live in a shared-memory ring of RING = PD + 3 slots filled by cp.async
+// (LDGSTS) PD planes ahead of the one being computed, so every thread keeps
+// several 8-byte loads in flight instead of one dependent load per plane.
+// Each T_n value is read from HBM once per step (plus tile halos, L2 hits).
+// ---------------------------------------------------------------------------
+constexpr int PD = 2;           // planes prefetched beyond z+1
+constexpr int RING = PD + 3;    // planes z-1, z, z+1 and PD more
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(uint32_t* smem, const uint32_t* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <bool COUPLED>
+__global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
+    const double* __restrict__ src, double* __restrict__ dst, ti64_stencil_args a,
+    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle, CoupledODE o) {
+  __shared__ double ring[RING][TY + 2][TX + 2];
+  __shared__ uint32_t iring[RING][TY];
+  const int64_t nx = a.nx, ny = a.ny, nz = a.nz;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int lane = tx;
+  const int64_t x = (int64_t)blockIdx.x * TX + tx;
+  const int64_t y = (int64_t)blockIdx.y * TY + ty;
+  const int64_t z0 = a.z_begin + (int64_t)blockIdx.z * zchunk;
+  const int64_t z1 = min(z0 + (int64_t)zchunk, a.z_end);
+  const bool in = x < nx && y < ny;
+  const int64_t plane = nx * ny;
+  const int64_t col = y * nx + x;
+  const double* sp = src + (-a.z_base) * plane + col;  // sp[z*plane] = T(z, y, x)
+  const double kf = c.kf;
+
+  // issue the copies of plane zz (interior + x/y halo; idle word per warp-row)
+  auto issue = [&](int64_t zz) {
+    if (zz >= 0 && zz < nz && zz >= a.z_base && zz < a.z_base + a.nz_stored) {
+      double(*P)[TX + 2] = ring[zz % RING];
+      const double* g = sp + zz * plane;
+      if (in) cp_async8(&P[ty + 1][tx + 1], g);
+      if (tx == 0 && x > 0 && y < ny) cp_async8(&P[ty + 1][0], g - 1);
+      if (tx == TX - 1 && x + 1 < nx && y < ny) cp_async8(&P[ty + 1][TX + 1], g + 1);
+      if (ty == 0 && y > 0 && x < nx) cp_async8(&P[0][tx + 1], g - nx);
+      if (ty == TY - 1 && y + 1 < ny && x < nx) cp_async8(&P[TY + 1][tx + 1], g + nx);
+      if (COUPLED && lane == 0 && y < ny && zz >= z0 && zz < z1)
+        cp_async4(&iring[zz % RING][ty], idle + ((zz * plane + y * nx + (x - lane)) >> 5));
+    }
+    cp_async_commit();
+  };
+
+  if (z0 >= z1) return;
+  for (int64_t zz = z0 - 1; zz <= z0 + PD; ++zz) issue(zz);
+  const unsigned gm =
+      COUPLED ? (((o.L >= 32) ? 0xffffffffu : ((1u << o.L) - 1u)) << (lane & ~(o.L - 1))) : 0u;
+
+  for (int64_t z = z0; z < z1; ++z) {
+    issue(z + 1 + PD);
+    cp_async_wait<PD>();  // planes <= z + 1 have landed (this thread's copies)
+    __syncthreads();          // ... and everyone's
+    const double(*P)[TX + 2] = ring[z % RING];
+    if (y < ny) {             // warp-uniform: one warp per x-row
+      double t_new = 0.0, t0 = 0.0;
+      if (in) {
+        t0 = P[ty + 1][tx + 1];
+        double flux = 0.0;
+        if (x > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty + 1][tx], t0)));
+        if (x + 1 < nx) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty + 1][tx + 2], t0)));
+        if (y > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty][tx + 1], t0)));
+        if (y + 1 < ny) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty + 2][tx + 1], t0)));
+        if (z > 0)
+          flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[(z - 1) % RING][ty + 1][tx + 1], t0)));
+        if (z + 1 < nz)
+          flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[(z + 1) % RING][ty + 1][tx + 1], t0)));
+        t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
+        if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
+        if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
+        dst[(z - a.z_base) * plane + col] = t_new;
+      }
+      if (COUPLED) {
+        // ---- kinetics of cell (z, y, x) with (T_n, T_{n+1}) = (t0, t_new) ----
+        const int64_t flat = z * plane + col;
+        const uint32_t bits = iring[z % RING][ty];
+        const bool was_idle = in && ((bits >> lane) & 1u);
+        const bool rest = o.rest_ok && was_idle && t0 < o.kp.t_as_end && t_new < o.kp.t_as_end;
+        if (!__all_sync(0xffffffffu, rest || !in)) {
+          bool touched = false;
+          bool now_idle = rest;
+          Seed sd;
+          sd.ac = 0;
+          sd.dr = 0;
+          sd.tr = 0.0;
+          if (in && !rest) {
+            double xs = f.x_alpha_s[flat], xm = f.x_alpha_m[flat], xb = f.x_beta[flat];
+            const int ac = f.seed_active[flat];
+            sd.ac = ac;
+            sd.dr = ac ? f.seed_direction[flat] : 0;
+            sd.tr = ac ? f.seed_tracked[flat] : 0.0;
+            touched = ac != 0;
+            double xaeq0 = xaeq_of(t0, o.kp, o.dv);
+            substep(xs, xm, xb, sd, t0, t_new, xaeq0, o.dt, o.kp, o.dv, o.cfg, touched);
+            f.x_alpha_s[flat] = xs;
+            f.x_alpha_m[flat] = xm;
+            f.x_beta[flat] = xb;
+            now_idle = idle_cell(xs, xm, xb, sd.ac);
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, touched && in);
+          if (in && (bal & gm)) {  // lane-group seed write-back (batch.py:687-692)
+            f.seed_tracked[flat] = sd.tr;
+            f.seed_active[flat] = (uint8_t)sd.ac;
+            f.seed_direction[flat] = (uint8_t)sd.dr;
+          }
+          const uint32_t nb = __ballot_sync(0xffffffffu, now_idle && in);
+          if (lane == 0 && nb != bits) idle[(z * plane + y * nx + (x - lane)) >> 5] = nb;
+        }
+      }
+    }
+    __syncthreads();  // slot of plane z-1 is refilled by the next iteration's issue
+  }
+  cp_async_wait<0>();
+}
+
+__global__ void idle_bits_init_kernel(ti64_fields f, uint32_t* idle, int64_t n) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w * 32 >= n) return;
+  uint32_t b = 0u;
+  for (int k = 0; k < 32; ++k) {
+    const int64_t i = w * 32 + k;
+    if (i < n && idle_cell(f.x_alpha_s[i], f.x_alpha_m[i], f.x_beta[i], f.seed_active[i]))
+      b |= 1u << k;
+  }
+  idle[w] = b;
+}
+
 }  // namespace
 
 void ti64_set_error(const std::string& msg);  // ti64_kernels.cu
@@ -217,7 +333,8 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
     const int zchunk = 16;
     dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TY - 1) / TY),
               (unsigned)((nzu + zchunk - 1) / zchunk));
-    stencil_built_kernel<<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk);
+    built_pipe_kernel<false><<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk,
+                                                          ti64_fields{}, nullptr, CoupledODE{});
   } else {
     const int64_t plane = a->nx * a->ny;
     const int64_t n = nzu * plane;
@@ -229,6 +346,62 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     ti64_set_error(std::string("ti64_stencil_step: ") + cudaGetErrorString(e));
+    return TI64_ECUDA;
+  }
+  ti64_set_error("");
+  return TI64_OK;
+}
+
+extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti64_fields* f,
+                                     uint32_t* idle_bits_d, const ti64_thermal* tp,
+                                     const ti64_stencil_args* a, const ti64_kparams* kp,
+                                     const ti64_icfg* cfg, int64_t lanes, int32_t init_bits,
+                                     void* stream) {
+  if (!tn_d || !tn1_d || !f || !idle_bits_d || !tp || !a || !kp || !cfg || tn_d == tn1_d ||
+      !a->all_built || a->losses_on || a->nx % 32 != 0 || a->z_base != 0 ||
+      a->nz_stored != a->nz || a->z_begin != 0 || a->z_end != a->z_top || a->z_top != a->nz ||
+      !(lanes == 1 || lanes == 2 || lanes == 4 || lanes == 8)) {
+    ti64_set_error("ti64_coupled_step: bad argument (needs a whole all-built grid, no losses, "
+                   "nx % 32 == 0)");
+    return TI64_EINVAL;
+  }
+  if (cfg->scheme != TI64_SCHEME_EXPLICIT) {
+    ti64_set_error("ti64_coupled_step: only the explicit scheme is implemented");
+    return TI64_ENOTSUP;
+  }
+  if (!(a->dt <= cfg->dt_sub_max * (1.0 + 1e-9))) {
+    ti64_set_error("ti64_coupled_step: dt above dt_sub_max (kinetics subcycling) unsupported");
+    return TI64_EINVAL;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = a->nx * a->ny * a->nz;
+  if (init_bits)
+    idle_bits_init_kernel<<<(unsigned)(((n + 31) / 32 + 255) / 256), 256, 0, st>>>(*f, idle_bits_d, n);
+  StencilConst c;
+  c.inv_rch2 = a->dt / (tp->rho_c * a->h * a->h);
+  c.inv_rch = a->dt / (tp->rho_c * a->h);
+  c.inv_rc = a->dt / tp->rho_c;
+  c.dk = tp->k_ms - tp->k_p;
+  c.t4inf = std::pow(tp->t_inf, 4.0);
+  const double kb = tp->k_p + 1.0 * c.dk;
+  c.kf = 2.0 * kb * kb / (kb + kb);
+  c.dliq = tp->t_liq - tp->t_sol;
+  c.src_coef = c.inv_rc * a->src_peak;
+  CoupledODE o;
+  o.kp = *kp;
+  o.dv = make_derived(*kp);
+  o.cfg = *cfg;
+  o.dt = a->dt;
+  o.L = (int)lanes;
+  o.rest_ok = kp->t_as_end <= kp->t_sol && kp->t_as_end <= kp->t_as_start && cfg->stuck_tol < 0.5;
+  const int zchunk = 16;
+  dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TY - 1) / TY),
+            (unsigned)((a->z_top + zchunk - 1) / zchunk));
+  built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
+                                                        idle_bits_d, o);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ti64_set_error(std::string("ti64_coupled_step: ") + cudaGetErrorString(e));
     return TI64_ECUDA;
   }
   ti64_set_error("");

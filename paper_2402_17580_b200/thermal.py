@@ -197,19 +197,66 @@ class CoupledDomain:
                                              device=dev), h, nz)
         self.shape = (nz, ny, nx)
         self.step = 0
+        self._idle_bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
+        self._bits_valid = False
         del np
 
     def run(self, n_steps, dt, beams, source, kinetics_params=None, integrator_config=None,
-            thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8):
-        """n_steps coupled steps; beams[k] = (x, y, power, on) of step k."""
+            thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8, fused=None):
+        """n_steps coupled steps; beams[k] = (x, y, power, on) of step k.
+
+        fused=True (default when nx % 32 == 0 and no losses) runs the single-pass
+        K4+kinetics kernel with ping-pong temperatures (bit-identical results);
+        fused=False issues step_thermal + step_all per step like the reference."""
         from .batch import step_all
         from .integrator import IntegratorConfig
         from .kinetics import DEFAULT_PARAMS
         kp = kinetics_params or DEFAULT_PARAMS
         cfg = integrator_config or IntegratorConfig(scheme="explicit")
+        nz, ny, nx = self.shape
+        if fused is None:
+            fused = nx % 32 == 0 and not losses and dt <= cfg.dt_sub_max * (1 + 1e-9)
+        if not fused:
+            self._bits_valid = False
+            for k in range(n_steps):
+                step_thermal(self.field, dt, thermal_params, source, beams[k], losses=losses,
+                             bottom_dirichlet=bottom, all_built=True)
+                step_all(self.fields, dt, kp, cfg, n_lanes=n_lanes)
+                self.step += 1
+            return self
+        return self._run_fused(n_steps, dt, beams, source, kp, cfg, thermal_params, bottom,
+                               n_lanes)
+
+    def _run_fused(self, n_steps, dt, beams, source, kp, cfg, thermal_params, bottom, n_lanes):
+        import ctypes as C
+        from . import _abi, _lib
+        lib = _lib.require()
+        dt_ok = stable_dt(self.field.h, thermal_params)
+        if dt > dt_ok * (1 + 1e-9):
+            raise ValueError(f"dt={dt:.3e} exceeds stability bound {dt_ok:.3e} s")
+        nz, ny, nx = self.shape
+        tp = _abi.thermal_from(thermal_params.kernel_tuple())
+        kpc = _abi.kparams_from(kp.kernel_tuple())
+        cfgc = _abi.icfg_from(cfg.kernel_tuple())
+        fs = self.fields.cstruct()
+        st = _lib.stream_handle()
+        cur, nxt = self.fields.temperature_old, self.fields.temperature_new
         for k in range(n_steps):
-            step_thermal(self.field, dt, thermal_params, source, beams[k], losses=losses,
-                         bottom_dirichlet=bottom, all_built=True)
-            step_all(self.fields, dt, kp, cfg, n_lanes=n_lanes)
+            a = _abi.stencil_args(nx, ny, nz, nz, dt, self.field.h, beam=beams[k],
+                                  source=source, losses=False, bottom=bottom, all_built=True)
+            rc = lib.ti64_coupled_step(_lib.ptr(cur), _lib.ptr(nxt), C.byref(fs),
+                                       _lib.ptr(self._idle_bits), C.byref(tp), C.byref(a),
+                                       C.byref(kpc), C.byref(cfgc), int(n_lanes),
+                                       0 if self._bits_valid else 1, st)
+            _lib.check(rc, "ti64_coupled_step")
+            self._bits_valid = True
+            cur, nxt = nxt, cur
             self.step += 1
+        # the reference ends a step with temperature_old == temperature_new
+        if cur is self.fields.temperature_new:
+            self.fields.temperature_old.copy_(cur)
+        else:
+            self.fields.temperature_new.copy_(cur)
+        self.fields.traffic_bytes += 72 * self.fields.n_points * n_steps
+        self.fields.steps_taken += n_steps
         return self

@@ -171,3 +171,25 @@ def test_slab_gpu_driver_single_rank_equals_coupled(env):
     ha, hb = a.fields.to_host(), b.fields.to_host()
     for k in ha:
         assert_bitwise(ha[k], hb[k], f"slab driver {k}")
+
+
+@pytest.mark.parametrize("lanes", [8, 1])
+def test_fused_coupled_equals_unfused(env, lanes):
+    """The single-pass K4+kinetics kernel (ping-pong T, idle bitmap) equals the
+    reference-shaped stencil + step_all sequence bit for bit."""
+    th = env["th"]
+    from paper_2402_17580_b200 import scanpath
+    nz, ny, nx, h, dt, nsteps = 14, 40, 64, 20e-6, 1e-6, 500
+    src = th.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=h)
+    segs = scanpath.serpentine((0.25e-3, 0.2e-3, 1.0e-3, 0.6e-3), 80e-6, 1.0, 87.5)
+    beams = scanpath.beam_schedule(segs, nsteps, dt)
+    a = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=h)
+    a.run(nsteps // 2, dt, beams, src, fused=False, n_lanes=lanes)
+    a.run(nsteps - nsteps // 2, dt, beams[nsteps // 2:], src, fused=False, n_lanes=lanes)
+    b = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=h)
+    b.run(nsteps // 2, dt, beams, src, fused=True, n_lanes=lanes)
+    b.run(nsteps - nsteps // 2, dt, beams[nsteps // 2:], src, fused=True, n_lanes=lanes)
+    ha, hb = a.fields.to_host(), b.fields.to_host()
+    assert ha["temperature_old"].max() > 1500.0
+    for k in ha:
+        assert_bitwise(ha[k], hb[k], f"fused {k}")
