@@ -178,108 +178,159 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+__device__ __forceinline__ void cp_async8s(unsigned sa, const double* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4s(unsigned sa, const uint32_t* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Each thread owns RY cells of its x column (rows y + r*TY), so the per-plane
+// bookkeeping (copies, waits, syncs, loop) is shared by RY cells.
+constexpr int RY = 2;
+constexpr int TYT = TY * RY;  // tile height in cells
+
+template <bool COUPLED>
+__device__ __forceinline__ void cell_kinetics(ti64_fields& f, uint32_t* __restrict__ idle,
+                                              const CoupledODE& o, int lane, bool in,
+                                              int64_t flat, uint32_t bits, double t0,
+                                              double t_new, unsigned gm) {
+  const bool was_idle = in && ((bits >> lane) & 1u);
+  const bool rest = o.rest_ok && was_idle && t0 < o.kp.t_as_end && t_new < o.kp.t_as_end;
+  if (__all_sync(0xffffffffu, rest || !in)) return;
+  bool touched = false;
+  bool now_idle = rest;
+  Seed sd;
+  sd.ac = 0;
+  sd.dr = 0;
+  sd.tr = 0.0;
+  if (in && !rest) {
+    double xs = f.x_alpha_s[flat], xm = f.x_alpha_m[flat], xb = f.x_beta[flat];
+    const int ac = f.seed_active[flat];
+    sd.ac = ac;
+    sd.dr = ac ? f.seed_direction[flat] : 0;
+    sd.tr = ac ? f.seed_tracked[flat] : 0.0;
+    touched = ac != 0;
+    double xaeq0 = xaeq_of(t0, o.kp, o.dv);
+    substep(xs, xm, xb, sd, t0, t_new, xaeq0, o.dt, o.kp, o.dv, o.cfg, touched);
+    f.x_alpha_s[flat] = xs;
+    f.x_alpha_m[flat] = xm;
+    f.x_beta[flat] = xb;
+    now_idle = idle_cell(xs, xm, xb, sd.ac);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, touched && in);
+  if (in && (bal & gm)) {  // lane-group seed write-back (batch.py:687-692)
+    f.seed_tracked[flat] = sd.tr;
+    f.seed_active[flat] = (uint8_t)sd.ac;
+    f.seed_direction[flat] = (uint8_t)sd.dr;
+  }
+  const uint32_t nb = __ballot_sync(0xffffffffu, now_idle && in);
+  if (lane == 0 && nb != bits) idle[(flat - lane) >> 5] = nb;
+}
+
 template <bool COUPLED>
 __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
     const double* __restrict__ src, double* __restrict__ dst, ti64_stencil_args a,
     StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle, CoupledODE o) {
-  __shared__ double ring[RING][TY + 2][TX + 2];
-  __shared__ uint32_t iring[RING][TY];
-  const int64_t nx = a.nx, ny = a.ny, nz = a.nz;
+  constexpr int W = TX + 2;              // smem row pitch
+  constexpr int SLOT = (TYT + 2) * W;    // doubles per ring slot
+  __shared__ double ring[RING * SLOT];
+  __shared__ uint32_t iring[RING * TYT];
+  const int nx = (int)a.nx, ny = (int)a.ny, nz = (int)a.nz;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int lane = tx;
-  const int64_t x = (int64_t)blockIdx.x * TX + tx;
-  const int64_t y = (int64_t)blockIdx.y * TY + ty;
-  const int64_t z0 = a.z_begin + (int64_t)blockIdx.z * zchunk;
-  const int64_t z1 = min(z0 + (int64_t)zchunk, a.z_end);
-  const bool in = x < nx && y < ny;
-  const int64_t plane = nx * ny;
-  const int64_t col = y * nx + x;
-  const double* sp = src + (-a.z_base) * plane + col;  // sp[z*plane] = T(z, y, x)
-  const double kf = c.kf;
+  const int x = blockIdx.x * TX + tx;
+  const int ybase = blockIdx.y * TYT;
+  const int z0 = (int)a.z_begin + blockIdx.z * zchunk;
+  const int z1 = min(z0 + zchunk, (int)a.z_end);
+  if (z0 >= z1) return;
+  const int64_t plane = (int64_t)nx * ny;
+  const int zlo = max(0, (int)a.z_base), zhi = min(nz, (int)(a.z_base + a.nz_stored));
+  const unsigned rbase = (unsigned)__cvta_generic_to_shared(ring);
+  const unsigned ibase = (unsigned)__cvta_generic_to_shared(iring);
+  // per owned row r: y, smem cell index, in-grid flag, halo duties
+  int yr[RY], cidx[RY];
+  bool in[RY], hl[RY], hr[RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    yr[r] = ybase + ty + r * TY;
+    cidx[r] = (ty + r * TY + 1) * W + tx + 1;
+    in[r] = x < nx && yr[r] < ny;
+    hl[r] = tx == 0 && x > 0 && yr[r] < ny;
+    hr[r] = tx == TX - 1 && x + 1 < nx && yr[r] < ny;
+  }
+  const bool hu = ty == 0 && ybase > 0 && x < nx;                  // row ybase-1
+  const bool hd = ty == TY - 1 && ybase + TYT < ny && x < nx;      // row ybase+TYT
+  const double* gcol = src + (-a.z_base) * plane + x;               // + z*plane + y*nx
 
-  // issue the copies of plane zz (interior + x/y halo; idle word per warp-row)
-  auto issue = [&](int64_t zz) {
-    if (zz >= 0 && zz < nz && zz >= a.z_base && zz < a.z_base + a.nz_stored) {
-      double(*P)[TX + 2] = ring[zz % RING];
-      const double* g = sp + zz * plane;
-      if (in) cp_async8(&P[ty + 1][tx + 1], g);
-      if (tx == 0 && x > 0 && y < ny) cp_async8(&P[ty + 1][0], g - 1);
-      if (tx == TX - 1 && x + 1 < nx && y < ny) cp_async8(&P[ty + 1][TX + 1], g + 1);
-      if (ty == 0 && y > 0 && x < nx) cp_async8(&P[0][tx + 1], g - nx);
-      if (ty == TY - 1 && y + 1 < ny && x < nx) cp_async8(&P[TY + 1][tx + 1], g + nx);
-      if (COUPLED && lane == 0 && y < ny && zz >= z0 && zz < z1)
-        cp_async4(&iring[zz % RING][ty], idle + ((zz * plane + y * nx + (x - lane)) >> 5));
+  auto issue = [&](int zz, int slot) {
+    if (zz >= zlo && zz < zhi) {
+      const double* g = gcol + (int64_t)zz * plane;
+      const unsigned so = rbase + 8u * (unsigned)(slot * SLOT);
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const unsigned sa = so + 8u * (unsigned)cidx[r];
+        const double* gr = g + (int64_t)yr[r] * nx;
+        if (in[r]) cp_async8s(sa, gr);
+        if (hl[r]) cp_async8s(sa - 8u, gr - 1);
+        if (hr[r]) cp_async8s(sa + 8u, gr + 1);
+      }
+      if (hu) cp_async8s(so + 8u * (unsigned)(tx + 1), g + (int64_t)(ybase - 1) * nx);
+      if (hd) cp_async8s(so + 8u * (unsigned)((TYT + 1) * W + tx + 1), g + (int64_t)(ybase + TYT) * nx);
+      if (COUPLED && lane == 0 && zz >= z0 && zz < z1) {
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+          if (yr[r] < ny)
+            cp_async4s(ibase + 4u * (unsigned)(slot * TYT + ty + r * TY),
+                       idle + (((int64_t)zz * plane + (int64_t)yr[r] * nx + (x - lane)) >> 5));
+      }
     }
     cp_async_commit();
   };
 
-  if (z0 >= z1) return;
-  for (int64_t zz = z0 - 1; zz <= z0 + PD; ++zz) issue(zz);
+  for (int k = 0; k <= PD + 1; ++k) issue(z0 - 1 + k, k);
+  int sm = 0, s0 = 1, sp1 = 2, si = PD + 2;  // slots of z-1, z, z+1, z+1+PD
+  const double kf = c.kf;
   const unsigned gm =
       COUPLED ? (((o.L >= 32) ? 0xffffffffu : ((1u << o.L) - 1u)) << (lane & ~(o.L - 1))) : 0u;
+  double* dcol = dst + (-a.z_base) * plane + x;
 
-  for (int64_t z = z0; z < z1; ++z) {
-    issue(z + 1 + PD);
+  for (int z = z0; z < z1; ++z) {
+    issue(z + 1 + PD, si);
     cp_async_wait<PD>();  // planes <= z + 1 have landed (this thread's copies)
-    __syncthreads();          // ... and everyone's
-    const double(*P)[TX + 2] = ring[z % RING];
-    if (y < ny) {             // warp-uniform: one warp per x-row
-      double t_new = 0.0, t0 = 0.0;
-      if (in) {
-        t0 = P[ty + 1][tx + 1];
-        double flux = 0.0;
-        if (x > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty + 1][tx], t0)));
-        if (x + 1 < nx) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty + 1][tx + 2], t0)));
-        if (y > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty][tx + 1], t0)));
-        if (y + 1 < ny) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[ty + 2][tx + 1], t0)));
-        if (z > 0)
-          flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[(z - 1) % RING][ty + 1][tx + 1], t0)));
-        if (z + 1 < nz)
-          flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[(z + 1) % RING][ty + 1][tx + 1], t0)));
-        t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
-        if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
-        if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
-        dst[(z - a.z_base) * plane + col] = t_new;
-      }
-      if (COUPLED) {
-        // ---- kinetics of cell (z, y, x) with (T_n, T_{n+1}) = (t0, t_new) ----
-        const int64_t flat = z * plane + col;
-        const uint32_t bits = iring[z % RING][ty];
-        const bool was_idle = in && ((bits >> lane) & 1u);
-        const bool rest = o.rest_ok && was_idle && t0 < o.kp.t_as_end && t_new < o.kp.t_as_end;
-        if (!__all_sync(0xffffffffu, rest || !in)) {
-          bool touched = false;
-          bool now_idle = rest;
-          Seed sd;
-          sd.ac = 0;
-          sd.dr = 0;
-          sd.tr = 0.0;
-          if (in && !rest) {
-            double xs = f.x_alpha_s[flat], xm = f.x_alpha_m[flat], xb = f.x_beta[flat];
-            const int ac = f.seed_active[flat];
-            sd.ac = ac;
-            sd.dr = ac ? f.seed_direction[flat] : 0;
-            sd.tr = ac ? f.seed_tracked[flat] : 0.0;
-            touched = ac != 0;
-            double xaeq0 = xaeq_of(t0, o.kp, o.dv);
-            substep(xs, xm, xb, sd, t0, t_new, xaeq0, o.dt, o.kp, o.dv, o.cfg, touched);
-            f.x_alpha_s[flat] = xs;
-            f.x_alpha_m[flat] = xm;
-            f.x_beta[flat] = xb;
-            now_idle = idle_cell(xs, xm, xb, sd.ac);
-          }
-          const unsigned bal = __ballot_sync(0xffffffffu, touched && in);
-          if (in && (bal & gm)) {  // lane-group seed write-back (batch.py:687-692)
-            f.seed_tracked[flat] = sd.tr;
-            f.seed_active[flat] = (uint8_t)sd.ac;
-            f.seed_direction[flat] = (uint8_t)sd.dr;
-          }
-          const uint32_t nb = __ballot_sync(0xffffffffu, now_idle && in);
-          if (lane == 0 && nb != bits) idle[(z * plane + y * nx + (x - lane)) >> 5] = nb;
+    __syncthreads();      // ... and everyone's
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      if (yr[r] < ny) {  // warp-uniform (one warp per x-row)
+        const int y = yr[r];
+        const double* P = ring + s0 * SLOT + cidx[r];
+        double t_new = 0.0, t0 = 0.0;
+        if (in[r]) {
+          t0 = P[0];
+          double flux = 0.0;
+          if (x > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[-1], t0)));
+          if (x + 1 < nx) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[1], t0)));
+          if (y > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[-W], t0)));
+          if (y + 1 < ny) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[W], t0)));
+          if (z > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sm * SLOT + cidx[r]], t0)));
+          if (z + 1 < nz)
+            flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sp1 * SLOT + cidx[r]], t0)));
+          t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
+          if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
+          if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
+          dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
         }
+        if (COUPLED)
+          cell_kinetics<COUPLED>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
+                                 iring[s0 * TYT + ty + r * TY], t0, t_new, gm);
       }
     }
     __syncthreads();  // slot of plane z-1 is refilled by the next iteration's issue
+    const int t = sm;
+    sm = s0;
+    s0 = sp1;
+    sp1 = (sp1 + 1 == RING) ? 0 : sp1 + 1;
+    si = t;
   }
   cp_async_wait<0>();
 }
@@ -331,7 +382,7 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
   if (nzu <= 0) return TI64_OK;
   if (a->all_built) {
     const int zchunk = 16;
-    dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TY - 1) / TY),
+    dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TYT - 1) / TYT),
               (unsigned)((nzu + zchunk - 1) / zchunk));
     built_pipe_kernel<false><<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk,
                                                           ti64_fields{}, nullptr, CoupledODE{});
@@ -395,7 +446,7 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   o.L = (int)lanes;
   o.rest_ok = kp->t_as_end <= kp->t_sol && kp->t_as_end <= kp->t_as_start && cfg->stuck_tol < 0.5;
   const int zchunk = 16;
-  dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TY - 1) / TY),
+  dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TYT - 1) / TYT),
             (unsigned)((a->z_top + zchunk - 1) / zchunk));
   built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
                                                         idle_bits_d, o);
