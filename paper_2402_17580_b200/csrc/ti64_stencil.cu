@@ -161,7 +161,13 @@ struct CoupledODE {
 // several 8-byte loads in flight instead of one dependent load per plane.
 // Each T_n value is read from HBM once per step (plus tile halos, L2 hits).
 // ---------------------------------------------------------------------------
-constexpr int PD = 2;           // planes prefetched beyond z+1
+#ifndef PD_DEF
+#define PD_DEF 2
+#endif
+#ifndef RY_DEF
+#define RY_DEF 2
+#endif
+constexpr int PD = PD_DEF;           // planes prefetched beyond z+1
 constexpr int RING = PD + 3;    // planes z-1, z, z+1 and PD more
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
@@ -187,7 +193,10 @@ __device__ __forceinline__ void cp_async4s(unsigned sa, const uint32_t* gmem) {
 
 // Each thread owns RY cells of its x column (rows y + r*TY), so the per-plane
 // bookkeeping (copies, waits, syncs, loop) is shared by RY cells.
-constexpr int RY = 2;
+constexpr int RY = RY_DEF;
+#ifndef ZCHUNK
+#define ZCHUNK 32
+#endif
 constexpr int TYT = TY * RY;  // tile height in cells
 
 template <bool COUPLED>
@@ -263,8 +272,9 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
   const bool hd = ty == TY - 1 && ybase + TYT < ny && x < nx;      // row ybase+TYT
   const double* gcol = src + (-a.z_base) * plane + x;               // + z*plane + y*nx
 
+  const int zmax = min(zhi, z1 + 1);  // plane z1 is the last one read (z+1 of z1-1)
   auto issue = [&](int zz, int slot) {
-    if (zz >= zlo && zz < zhi) {
+    if (zz >= zlo && zz < zmax) {
       const double* g = gcol + (int64_t)zz * plane;
       const unsigned so = rbase + 8u * (unsigned)(slot * SLOT);
 #pragma unroll
@@ -381,7 +391,7 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
   const int64_t nzu = a->z_end - a->z_begin;
   if (nzu <= 0) return TI64_OK;
   if (a->all_built) {
-    const int zchunk = 16;
+    const int zchunk = ZCHUNK;
     dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TYT - 1) / TYT),
               (unsigned)((nzu + zchunk - 1) / zchunk));
     built_pipe_kernel<false><<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk,
@@ -445,7 +455,7 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   o.dt = a->dt;
   o.L = (int)lanes;
   o.rest_ok = kp->t_as_end <= kp->t_sol && kp->t_as_end <= kp->t_as_start && cfg->stuck_tol < 0.5;
-  const int zchunk = 16;
+  const int zchunk = ZCHUNK;
   dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TYT - 1) / TYT),
             (unsigned)((a->z_top + zchunk - 1) / zchunk));
   built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
