@@ -16,9 +16,14 @@
 //    the post-sweep temperatures.
 // Face order x-, x+, y-, y+, z-, z+ and every association follow the
 // reference (thermal.py:228-273); missing / inactive faces are skipped.
+#include <cuda.h>  // CUtensorMap (types only; the encoder comes via cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/ti64_b200.h"
@@ -345,6 +350,256 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// TMA variant: one elected thread moves each (TX+2) x (TYT+2) plane box (tile
+// plus x/y halo, out-of-range cells zero-filled) into the shared-memory ring
+// with cp.async.bulk.tensor; an mbarrier per slot carries the transaction
+// count.  The other threads only compute, so the per-cell instruction count
+// is the stencil arithmetic itself.
+// ---------------------------------------------------------------------------
+// the box starts at x0 - 2: TMA needs the innermost start coordinate 16-byte
+// aligned (measured: an odd double offset faults), so 2 halo columns on the
+// left (one unused) and 2 on the right keep the box 36 doubles = 288 B wide
+constexpr int BOX_X = TX + 4, BOX_Y = TYT + 2;
+constexpr int BOX_BYTES = BOX_X * BOX_Y * 8;
+constexpr int SLOT_BYTES = (BOX_BYTES + 127) / 128 * 128;
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+// bounded wait: a transaction that never lands traps (kernel error) instead
+// of hanging the GPU
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 4000000000LL) {  // ~2 s: a transaction never landed
+      unsigned other;
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          " selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(other)
+          : "r"(bar), "r"(parity ^ 1u));
+      if (threadIdx.x == 0 && threadIdx.y == 0)
+        printf("ti64 TMA wait timeout: block (%d,%d,%d) bar %u parity %u other-phase-done %u\n",
+               blockIdx.x, blockIdx.y, blockIdx.z, bar, parity, other);
+#ifdef TI64_TMA_DEBUG
+      return;
+#else
+      __trap();
+#endif
+    }
+  }
+}
+__device__ __forceinline__ void tma_load_3d(unsigned dst, uint64_t desc, int c0, int c1, int c2,
+                                            unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+template <bool COUPLED>
+__global__ void __launch_bounds__(TX* TY) built_tma_kernel(
+    const __grid_constant__ CUtensorMap tmap, double* __restrict__ dst, ti64_stencil_args a,
+    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle, CoupledODE o) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);  // RING slots of SLOT_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT_BYTES);
+  uint32_t* iring = reinterpret_cast<uint32_t*>(smem_raw + RING * SLOT_BYTES + RING * 8);
+  constexpr int SLOTD = SLOT_BYTES / 8;  // doubles per slot
+  constexpr int W = BOX_X;
+  const int nx = (int)a.nx, ny = (int)a.ny, nz = (int)a.nz;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int lane = tx;
+  const bool leader = tx == 0 && ty == 0;
+  const int x0 = blockIdx.x * TX, ybase = blockIdx.y * TYT;
+  const int x = x0 + tx;
+  const int z0 = (int)a.z_begin + blockIdx.z * zchunk;
+  const int z1 = min(z0 + zchunk, (int)a.z_end);
+  if (z0 >= z1) return;
+  const int64_t plane = (int64_t)nx * ny;
+  const int zlo = max(0, (int)a.z_base), zhi = min(nz, (int)(a.z_base + a.nz_stored));
+  const int zmax = min(zhi, z1 + 1);
+  // the descriptor address is taken here, in the kernel body: a lambda that
+  // captured the __grid_constant__ parameter by reference would copy it to
+  // local memory, where TMA cannot read it (the load then never lands)
+  const uint64_t desc = reinterpret_cast<uint64_t>(&tmap);
+  const unsigned rbase = (unsigned)__cvta_generic_to_shared(ring);
+  const unsigned bbase = (unsigned)__cvta_generic_to_shared(bars);
+  const unsigned ibase = (unsigned)__cvta_generic_to_shared(iring);
+  int yr[RY], cidx[RY];
+  bool in[RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    yr[r] = ybase + ty + r * TY;
+    cidx[r] = (ty + r * TY + 1) * W + tx + 2;
+    in[r] = x < nx && yr[r] < ny;
+  }
+  if (leader) {
+    for (int k = 0; k < RING; ++k) mbar_init(bbase + 8u * k, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // plane zz lives in slot (zz - (z0 - 1)) % RING
+  auto issue = [&](int zz, int slot) {
+    if (leader && zz >= zlo && zz < zmax) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      const unsigned bar = bbase + 8u * slot;
+      mbar_expect_tx(bar, (unsigned)BOX_BYTES);
+      tma_load_3d(rbase + (unsigned)(slot * SLOT_BYTES), desc, x0 - 2, ybase - 1,
+                  zz - (int)a.z_base, bar);
+    }
+    if (COUPLED) {
+      if (lane == 0 && zz >= z0 && zz < z1) {
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+          if (yr[r] < ny)
+            cp_async4s(ibase + 4u * (unsigned)(slot * TYT + ty + r * TY),
+                       idle + (((int64_t)zz * plane + (int64_t)yr[r] * nx + x0) >> 5));
+      }
+      cp_async_commit();
+    }
+  };
+  // per-slot phase parity of the next completion to wait for: loads and waits
+  // pair up one-to-one per slot (planes outside the grid are neither issued
+  // nor waited), so a bit flip per completed wait tracks the phase
+  unsigned phase = 0u;
+  auto wait_plane = [&](int zz, int slot) {
+    if (zz >= zlo && zz < zmax) {
+      mbar_wait(bbase + 8u * slot, (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+    }
+  };
+
+  for (int k = 0; k <= PD + 1; ++k) issue(z0 - 1 + k, k);
+  int sm = 0, s0 = 1, sp1 = 2, si = PD + 2;
+  wait_plane(z0 - 1, 0);
+  wait_plane(z0, 1);
+  const double kf = c.kf;
+  const unsigned gm =
+      COUPLED ? (((o.L >= 32) ? 0xffffffffu : ((1u << o.L) - 1u)) << (lane & ~(o.L - 1))) : 0u;
+  double* dcol = dst + (-a.z_base) * plane + x;
+
+  for (int z = z0; z < z1; ++z) {
+    issue(z + 1 + PD, si);
+    wait_plane(z + 1, sp1);
+    if (COUPLED) {
+      cp_async_wait<PD>();
+      __syncthreads();
+    }
+    double tm_[RY];
+#pragma unroll
+    for (int r = 0; r < RY; ++r) tm_[r] = 0.0;
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      if (yr[r] < ny) {  // warp-uniform (one warp per x-row)
+        const int y = yr[r];
+        const double* P = ring + s0 * SLOTD + cidx[r];
+        double t_new = 0.0, t0 = 0.0;
+        if (in[r]) {
+          t0 = P[0];
+          double flux = 0.0;
+          if (x > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[-1], t0)));
+          if (x + 1 < nx) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[1], t0)));
+          if (y > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[-W], t0)));
+          if (y + 1 < ny) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[W], t0)));
+          if (z > 0) flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sm * SLOTD + cidx[r]], t0)));
+          if (z + 1 < nz)
+            flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sp1 * SLOTD + cidx[r]], t0)));
+          t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
+          if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
+          if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
+          dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
+        }
+        if (COUPLED)
+          cell_kinetics<COUPLED>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
+                                 iring[s0 * TYT + ty + r * TY], t0, t_new, gm);
+      }
+    }
+    (void)tm_;
+    __syncthreads();  // every thread is done with slot sm before it is refilled
+    const int t = sm;
+    sm = s0;
+    s0 = sp1;
+    sp1 = (sp1 + 1 == RING) ? 0 : sp1 + 1;
+    si = t;
+  }
+  if (COUPLED) cp_async_wait<0>();
+}
+
+// --- host: tensor-map encoder through the runtime's driver entry point ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// 3D map over the stored planes (x fastest); false when TMA cannot be used
+bool make_plane_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t nzs) {
+  EncodeTiledFn enc = encoder();
+  // the box must fit inside the tensor (a box wider than the grid stalls)
+  if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || (nx * 8) % 16 != 0 || nx < BOX_X ||
+      ny < BOX_Y ||
+      nx > (1LL << 31) || ny > (1LL << 31) || nzs > (1LL << 31))
+    return false;
+  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nzs};
+  cuuint64_t strides[2] = {(cuuint64_t)(nx * 8), (cuuint64_t)(nx * ny * 8)};
+  cuuint32_t box[3] = {(cuuint32_t)BOX_X, (cuuint32_t)BOX_Y, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  std::memset(m, 0, sizeof(*m));
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr int TMA_SMEM = RING * SLOT_BYTES + RING * 8 + RING * TYT * 4;
+
+template <bool COUPLED>
+bool launch_built(const double* src, double* dst, const ti64_stencil_args& a,
+                  const StencilConst& c, ti64_fields f, uint32_t* idle, const CoupledODE& o,
+                  dim3 grid, int zchunk, cudaStream_t st) {
+  CUtensorMap m;
+  if (!make_plane_map(&m, src, a.nx, a.ny, a.nz_stored)) return false;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(built_tma_kernel<COUPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TMA_SMEM);
+    attr_set = true;
+  }
+  built_tma_kernel<COUPLED><<<grid, dim3(TX, TY), TMA_SMEM, st>>>(m, dst, a, c, zchunk, f, idle, o);
+  return true;
+}
+
 __global__ void idle_bits_init_kernel(ti64_fields f, uint32_t* idle, int64_t n) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w * 32 >= n) return;
@@ -360,6 +615,18 @@ __global__ void idle_bits_init_kernel(ti64_fields f, uint32_t* idle, int64_t n) 
 }  // namespace
 
 void ti64_set_error(const std::string& msg);  // ti64_kernels.cu
+
+namespace {
+// TI64_NO_TMA=1 forces the cp.async pipeline (A/B comparisons, parity tests)
+bool use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TI64_NO_TMA");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+}  // namespace
 
 extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double* rc_d,
                                      const uint8_t* state_d, const ti64_thermal* tp,
@@ -394,8 +661,10 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
     const int zchunk = ZCHUNK;
     dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TYT - 1) / TYT),
               (unsigned)((nzu + zchunk - 1) / zchunk));
-    built_pipe_kernel<false><<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk,
-                                                          ti64_fields{}, nullptr, CoupledODE{});
+    if (!use_tma() || !launch_built<false>(src_d, dst_d, *a, c, ti64_fields{}, nullptr,
+                                           CoupledODE{}, grid, zchunk, st))
+      built_pipe_kernel<false><<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk,
+                                                            ti64_fields{}, nullptr, CoupledODE{});
   } else {
     const int64_t plane = a->nx * a->ny;
     const int64_t n = nzu * plane;
@@ -458,8 +727,9 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   const int zchunk = ZCHUNK;
   dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TYT - 1) / TYT),
             (unsigned)((a->z_top + zchunk - 1) / zchunk));
-  built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
-                                                        idle_bits_d, o);
+  if (!use_tma() || !launch_built<true>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, grid, zchunk, st))
+    built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
+                                                          idle_bits_d, o);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     ti64_set_error(std::string("ti64_coupled_step: ") + cudaGetErrorString(e));

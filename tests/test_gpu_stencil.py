@@ -193,3 +193,22 @@ def test_fused_coupled_equals_unfused(env, lanes):
     assert ha["temperature_old"].max() > 1500.0
     for k in ha:
         assert_bitwise(ha[k], hb[k], f"fused {k}")
+
+
+def test_cp_async_pipeline_equals_tma(env, tmp_path):
+    """Both K4 pipelines (TMA default; cp.async with TI64_NO_TMA=1) give the
+    same bits, for the stencil and the fused coupled step."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    outs = []
+    for flag in ("0", "1"):
+        out = tmp_path / f"ab_{flag}.npz"
+        e = dict(os.environ, TI64_NO_TMA=flag)
+        subprocess.run([sys.executable, str(root / "tools" / "stencil_ab.py"), str(out)],
+                       env=e, check=True, cwd=root)
+        outs.append(np.load(out))
+    for k in outs[0].files:
+        assert_bitwise(outs[0][k], outs[1][k], f"tma vs cp.async {k}")
