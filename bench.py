@@ -199,6 +199,67 @@ def measure_fp64_peak(torch, lib, stream):
     return best
 
 
+def _time_dev(torch, fn, reps=5, flush=None):
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    return sorted(ts)[len(ts) // 2]
+
+
+def measure_extra(torch, pkg, dev):
+    """Secondary evidence (not the headline): the HBM-bound stencil K4 and the
+    fused config-3 step at 512x512x256, and the all-active pure-ODE configs 2
+    and 4 on a 2^22-point shard for 2000 steps (per-GPU, fp64)."""
+    from paper_2402_17580_b200 import thermal as th, scanpath
+    hbm = 6538.0
+    try:
+        hbm = float(json.load(open(ROOT / "MEASURED_PEAKS.json"))["hbm_gbs"])
+    except Exception:
+        pass
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    out = {}
+    nz, ny, nx = 256, 512, 512
+    n = nz * ny * nx
+    dom = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=20e-6, device=dev)
+    src = th.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=20e-6)
+    segs = scanpath.serpentine((1e-3, 1e-3, 9.24e-3, 9.24e-3), 80e-6, 1.0, 0.35 * 250.0)
+    beams = scanpath.beam_schedule(segs, 400, 1e-6)
+    dom.run(100, 1e-6, beams, src, fused=True)
+    k = [100]
+
+    def stencil():
+        th.step_thermal(dom.field, 1e-6, th.DEFAULT_THERMAL, src, beams[k[0]], losses=False,
+                        bottom_dirichlet=353.0, all_built=True)
+    t = _time_dev(torch, stencil, 7, flush)
+    out["stencil_K4_config3_grid"] = {
+        "cells": n, "us": t * 1e6, "GB/s": 16 * n / t / 1e9, "frac_of_measured_hbm": 16 * n / t / 1e9 / hbm,
+        "bytes_model": "16 B/cell (8 read T_n + 8 write T_n+1)", "pipeline": "TMA + mbarrier ring"}
+
+    def coupled():
+        dom.run(10, 1e-6, beams[k[0]:], src, fused=True)
+        k[0] += 10
+    t = _time_dev(torch, coupled, 5) / 10
+    out["config3_fused_coupled_step"] = {"cells": n, "ms_per_step": t * 1e3,
+                                        "cell_steps_per_s": n / t,
+                                        "job_estimate_s": 20000 * t}
+    del dom
+    for c in (2, 4):
+        src_c = pkg.source_for_config(c)
+        f = pkg.init_from_source(src_c, 1 << 22, device=dev)
+        pkg.advance(f, 200, src_c, snapshot_every=1000)
+        t = _time_dev(torch, lambda: pkg.advance(f.copy(), 2000, src_c, step0=200,
+                                                snapshot_every=1000), 1)
+        out[f"config{c}_shard_2^22x2000"] = {"point_updates_per_s": (1 << 22) * 2000 / t}
+    return out
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -297,6 +358,7 @@ def run_b200(args):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world * upd_job / float(e2e_t.item())
 
+    extra = measure_extra(torch, pkg, dev) if (rank == 0 and not args.quick) else None
     if rank == 0:
         peak = measure_fp64_peak(torch, lib, stream)
         per_launch_s = total_s / (args.steps * (nsteps // SNAP_EVERY))
@@ -325,6 +387,7 @@ def run_b200(args):
             "clocks": clocks,
             "cpu_baseline": None if cpu is None else
             {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "extra": extra,
             "checks": {"counted_equals_timed_bitwise": bool(same),
                        "sums_last": [float(x) for x in sums_last[-1].cpu().numpy()],
                        "totals": totals},
@@ -345,6 +408,7 @@ def main():
     ap.add_argument("--job-steps", type=int, default=JOB_STEPS)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip the secondary measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
