@@ -54,6 +54,8 @@ def lib():
         L.oracle_fast_pow.restype = None
         L.oracle_run_range.argtypes = [P, I64, I64, I64, I64, D, P, P]
         L.oracle_run_range.restype = I64
+        L.oracle_run_range2.argtypes = [P, I64, I64, I64, I64, D, P, P, I32, P]
+        L.oracle_run_range2.restype = I64
         L.oracle_step_all.argtypes = [P, I64, I64, I64, D, P, P, I32]
         L.oracle_step_all.restype = I64
         L.oracle_num_substeps.argtypes = [D, D]
@@ -155,6 +157,19 @@ def run_range(fields, kp, cfg, lanes=8, nsub=1, dt_sub=2e-5, start=0, stop=None)
     k, c = _abi.kparams_from(kp), _abi.icfg_from(cfg)
     return int(lib().oracle_run_range(C.byref(fs), start, stop, lanes, nsub,
                                       float(dt_sub), C.byref(k), C.byref(c)))
+
+
+def run_range_cn(fields, kp, cfg, lanes=8, nsub=1, dt_sub=0.01, record_iters=True):
+    """batch.run_range for either scheme over all points (single sweep, like
+    step_all with threads=1); returns (rc, iters)."""
+    n = fields.n_points
+    iters = np.zeros(n, np.int64)
+    fs = fields.cstruct()
+    k, c = _abi.kparams_from(kp), _abi.icfg_from(cfg)
+    rc = int(lib().oracle_run_range2(C.byref(fs), 0, n, lanes, nsub, float(dt_sub),
+                                     C.byref(k), C.byref(c), int(bool(record_iters)),
+                                     _p(iters)))
+    return rc, iters
 
 
 def num_substeps(dt, dt_sub_max):

@@ -330,21 +330,93 @@ static int seed_pass(int L, double* lxs, double* lxm, double* lxb, double* ltr,
   return n_seed;
 }
 
-/* batch.py:467-695 _range_body, explicit=True (the scheme the B200 path
- * implements; pieces stay 1 because the explicit step never halves). */
-int64_t oracle_run_range(const ti64_fields* f, int64_t start, int64_t stop,
-                         int64_t lanes, int64_t nsub, double dt_sub,
-                         const ti64_kparams* kp, const ti64_icfg* cfg) {
-  if (cfg->scheme != TI64_SCHEME_EXPLICIT) return TI64_ENOTSUP;
+/* batch.py:357-416 _cn_substep: Crank-Nicolson fixed point with per-lane
+ * WRMS freeze; returns all-converged, writes the iteration count */
+static int cn_substep(int L, const double* lxs, const double* lxm, const double* pt1,
+                      const double* xsol1, const double* xaeq1, const double* kas1,
+                      const double* xmeqb1, const double* dsn, const double* dmn, double* dsi,
+                      double* dmi, double* dsx, double* dmx, double* cxs, double* cxm,
+                      double* cxb, double* pxs, double* pa, double* pb, double* pc, double* pd,
+                      double* exs, double* exm, double* exb, double* sxs, double* sxm,
+                      double* sxb, uint8_t* conv, double* itc, double dt,
+                      const ti64_icfg* cfg, const ti64_kparams* kp, int* iters_out) {
+  int any_form = 0, any_reg = 0;
+  for (int j = 0; j < L; ++j) {
+    any_form += pt1[j] < kp->t_am_start;
+    any_reg += pt1[j] > kp->t_as_start;
+    conv[j] = 0;
+  }
+  lane_corrections(L, lxs, lxm, pt1, xaeq1, xsol1, xmeqb1, any_form > 0, any_reg > 0, cxs, cxm,
+                   cxb, kp);
+  lane_rates(L, cxs, cxm, xaeq1, kas1, dsi, dmi, pxs, pa, pb, pc, pd, kp);
+  double half = 0.5 * dt;
+  int iters = 0;
+  for (;;) {
+    for (int j = 0; j < L; ++j) {
+      exs[j] = lxs[j] + half * (dsi[j] + dsn[j]);
+      exm[j] = lxm[j] + half * (dmi[j] + dmn[j]);
+    }
+    lane_corrections(L, exs, exm, pt1, xaeq1, xsol1, xmeqb1, any_form > 0, any_reg > 0, cxs,
+                     cxm, cxb, kp);
+    lane_rates(L, cxs, cxm, xaeq1, kas1, dsx, dmx, pxs, pa, pb, pc, pd, kp);
+    iters += 1;
+    int n_open = 0;
+    for (int j = 0; j < L; ++j) {
+      if (conv[j] == 0) {
+        double rs = half * (dsx[j] - dsi[j]);
+        double rm = half * (dmx[j] - dmi[j]);
+        double ws = 1.0 / (cfg->eps_abs + fabs(cxs[j]) * cfg->eps_rel);
+        double wm = 1.0 / (cfg->eps_abs + fabs(cxm[j]) * cfg->eps_rel);
+        double e = 0.5 * ((rs * ws) * (rs * ws) + (rm * wm) * (rm * wm));
+        sxs[j] = cxs[j];
+        sxm[j] = cxm[j];
+        sxb[j] = cxb[j];
+        dsi[j] = dsx[j];
+        dmi[j] = dmx[j];
+        itc[j] += 1.0;
+        if (e < 1.0)
+          conv[j] = 1;
+        else
+          n_open += 1;
+      }
+    }
+    if (n_open == 0 || iters >= cfg->max_fixed_point_iters) {
+      for (int j = 0; j < L; ++j) {
+        exs[j] = sxs[j];
+        exm[j] = sxm[j];
+        exb[j] = sxb[j];
+      }
+      *iters_out = iters;
+      return n_open == 0;
+    }
+  }
+}
+
+/* batch.py:467-695 _range_body, both schemes (explicit: pieces stay 1 since
+ * the explicit step never fails; implicit: halving retries with state
+ * rollback, batch.py:568-674).  iters_out (may be NULL) receives the
+ * per-point implicit iteration counts when record_iters. */
+int64_t oracle_run_range2(const ti64_fields* f, int64_t start, int64_t stop, int64_t lanes,
+                          int64_t nsub, double dt_sub, const ti64_kparams* kp,
+                          const ti64_icfg* cfg, int32_t record_iters, int64_t* iters_out) {
   if (lanes < 1 || lanes > MAXL) return TI64_EINVAL;
+  const int explicit_ = cfg->scheme == TI64_SCHEME_EXPLICIT;
   const int L = (int)lanes;
   double lxs[MAXL], lxm[MAXL], lxb[MAXL], lt0[MAXL], lt1[MAXL], st0[MAXL], st1[MAXL];
+  double pt0[MAXL], pt1[MAXL];
   double g1[MAXL], xsol1[MAXL], xaeq1[MAXL], kas1[MAXL], xmeqb1[MAXL];
   double xaeq0[MAXL], kas0[MAXL], ltr[MAXL], dsn[MAXL], dmn[MAXL];
+  double dsi[MAXL], dmi[MAXL], dsx[MAXL], dmx[MAXL], cxs[MAXL], cxm[MAXL], cxb[MAXL];
   double pxs[MAXL] = {0}, pa[MAXL] = {0}, pb[MAXL] = {0}, pc[MAXL] = {0}, pd[MAXL] = {0};
-  double exs[MAXL], exm[MAXL], exb[MAXL];
-  uint8_t lac[MAXL], ldr[MAXL];
+  double exs[MAXL], exm[MAXL], exb[MAXL], sxs[MAXL], sxm[MAXL], sxb[MAXL], itc[MAXL];
+  double bxs[MAXL], bxm[MAXL], bxb[MAXL], btr[MAXL];
+  uint8_t lac[MAXL], ldr[MAXL], bac[MAXL], bdr[MAXL], conv[MAXL];
   memset(xmeqb1, 0, sizeof xmeqb1);
+  memset(xaeq1, 0, sizeof xaeq1);
+  memset(kas1, 0, sizeof kas1);
+  memset(sxs, 0, sizeof sxs);
+  memset(sxm, 0, sizeof sxm);
+  memset(sxb, 0, sizeof sxb);
   const double inv_nsub = 1.0 / (double)nsub;
   const double stuck_tol = cfg->stuck_tol;
   for (int64_t base = start; base < stop; base += lanes) {
@@ -363,8 +435,10 @@ int64_t oracle_run_range(const ti64_fields* f, int64_t start, int64_t stop,
       lac[j] = ac;
       ldr[j] = ac != 0 ? f->seed_direction[i] : 0;
       ltr[j] = ac != 0 ? f->seed_tracked[i] : 0.0;
+      if (!explicit_) itc[j] = 0.0;
     }
     int seed_out = n_seed_in > 0;
+    int failed = 0;
     for (int64_t k = 0; k < nsub; ++k) {
       int last_sub = k == nsub - 1;
       const double *s0v, *s1v;
@@ -382,50 +456,107 @@ int64_t oracle_run_range(const ti64_fields* f, int64_t start, int64_t stop,
         s0v = st0;
         s1v = st1;
       }
-      /* pieces == 1: p0v = s0v, p1v = s1v (batch.py:584-586) */
-      if (k == 0) {
-        lane_tfuncs_rates(L, s0v, xaeq0, kas0, kp);
-      } else {
+      if (!explicit_)
         for (int j = 0; j < L; ++j) {
-          xaeq0[j] = xaeq1[j];
-          kas0[j] = kas1[j];
+          bxs[j] = lxs[j];
+          bxm[j] = lxm[j];
+          bxb[j] = lxb[j];
+          btr[j] = ltr[j];
+          bac[j] = lac[j];
+          bdr[j] = ldr[j];
+        }
+      int halv = 0;
+      for (;;) {
+        int64_t pieces = (int64_t)1 << halv;
+        double inv_p = 1.0 / (double)pieces;
+        int ok = 1;
+        for (int64_t p = 0; p < pieces; ++p) {
+          const double *p0v, *p1v;
+          if (pieces == 1) {
+            p0v = s0v;
+            p1v = s1v;
+          } else {
+            double pf0 = (double)p * inv_p;
+            double pf1 = (double)(p + 1) * inv_p;
+            int last_p = p == pieces - 1;
+            for (int j = 0; j < L; ++j) {
+              double dts = s1v[j] - s0v[j];
+              pt0[j] = s0v[j] + dts * pf0;
+              pt1[j] = last_p ? s1v[j] : s0v[j] + dts * pf1;
+            }
+            p0v = pt0;
+            p1v = pt1;
+          }
+          if (k == 0 && p == 0) {
+            lane_tfuncs_rates(L, p0v, xaeq0, kas0, kp);
+          } else if (halv == 0 || p > 0) {
+            for (int j = 0; j < L; ++j) {
+              xaeq0[j] = xaeq1[j];
+              kas0[j] = kas1[j];
+            }
+          } else {
+            lane_tfuncs_rates(L, p0v, xaeq0, kas0, kp);
+          }
+          lane_tfuncs(L, p1v, g1, xsol1, xaeq1, kas1, kp);
+          int n_form = 0, n_reg = 0, n_watch = 0;
+          for (int j = 0; j < L; ++j) {
+            n_form += p1v[j] < kp->t_am_start;
+            n_reg += p1v[j] > kp->t_as_start;
+            int watch = (lac[j] != 0) |
+                        ((fabs(lxm[j]) <= stuck_tol) &
+                         ((fabs(lxs[j]) <= stuck_tol) | (fabs(lxs[j] - XA_MAX) <= stuck_tol)));
+            n_watch += watch;
+          }
+          if (n_form > 0) lane_xmeq_base(L, p1v, xmeqb1, kp);
+          int n_seed = 0;
+          if (n_watch > 0)
+            n_seed = seed_pass(L, lxs, lxm, lxb, ltr, lac, ldr, p1v, g1, xsol1, xaeq1, kas1,
+                               exs, exm, exb, 0.0, cfg, kp, 0);
+          double dt_p = dt_sub * inv_p;
+          int its = 0;
+          if (n_seed < L) {
+            lane_rates(L, lxs, lxm, xaeq0, kas0, dsn, dmn, pxs, pa, pb, pc, pd, kp);
+            if (explicit_) {
+              for (int j = 0; j < L; ++j) {
+                exs[j] = lxs[j] + dt_p * dsn[j];
+                exm[j] = lxm[j] + dt_p * dmn[j];
+              }
+              lane_corrections(L, exs, exm, p1v, xaeq1, xsol1, xmeqb1, n_form > 0, n_reg > 0,
+                               exs, exm, exb, kp);
+            } else {
+              ok = cn_substep(L, lxs, lxm, p1v, xsol1, xaeq1, kas1, xmeqb1, dsn, dmn, dsi, dmi,
+                              dsx, dmx, cxs, cxm, cxb, pxs, pa, pb, pc, pd, exs, exm, exb, sxs,
+                              sxm, sxb, conv, itc, dt_p, cfg, kp, &its);
+            }
+          }
+          if (n_seed > 0) {
+            seed_pass(L, lxs, lxm, lxb, ltr, lac, ldr, p1v, g1, xsol1, xaeq1, kas1, exs, exm,
+                      exb, dt_p, cfg, kp, 1);
+            seed_out = 1;
+          }
+          for (int j = 0; j < L; ++j) {
+            lxs[j] = exs[j];
+            lxm[j] = exm[j];
+            lxb[j] = exb[j];
+          }
+          if (!ok) break;
+        }
+        if (ok) break;
+        halv += 1;
+        if (halv > cfg->max_halvings) {
+          failed = 1;
+          break;
+        }
+        for (int j = 0; j < L; ++j) {
+          lxs[j] = bxs[j];
+          lxm[j] = bxm[j];
+          lxb[j] = bxb[j];
+          ltr[j] = btr[j];
+          lac[j] = bac[j];
+          ldr[j] = bdr[j];
         }
       }
-      lane_tfuncs(L, s1v, g1, xsol1, xaeq1, kas1, kp);
-      int n_form = 0, n_reg = 0, n_watch = 0;
-      for (int j = 0; j < L; ++j) {
-        n_form += s1v[j] < kp->t_am_start;
-        n_reg += s1v[j] > kp->t_as_start;
-        int watch = (lac[j] != 0) |
-                    ((fabs(lxm[j]) <= stuck_tol) &
-                     ((fabs(lxs[j]) <= stuck_tol) | (fabs(lxs[j] - XA_MAX) <= stuck_tol)));
-        n_watch += watch;
-      }
-      if (n_form > 0) lane_xmeq_base(L, s1v, xmeqb1, kp);
-      int n_seed = 0;
-      if (n_watch > 0)
-        n_seed = seed_pass(L, lxs, lxm, lxb, ltr, lac, ldr, s1v, g1, xsol1, xaeq1,
-                           kas1, exs, exm, exb, 0.0, cfg, kp, 0);
-      double dt_p = dt_sub * 1.0; /* inv_p == 1.0 */
-      if (n_seed < L) {
-        lane_rates(L, lxs, lxm, xaeq0, kas0, dsn, dmn, pxs, pa, pb, pc, pd, kp);
-        for (int j = 0; j < L; ++j) {
-          exs[j] = lxs[j] + dt_p * dsn[j];
-          exm[j] = lxm[j] + dt_p * dmn[j];
-        }
-        lane_corrections(L, exs, exm, s1v, xaeq1, xsol1, xmeqb1, n_form > 0,
-                         n_reg > 0, exs, exm, exb, kp);
-      }
-      if (n_seed > 0) {
-        seed_pass(L, lxs, lxm, lxb, ltr, lac, ldr, s1v, g1, xsol1, xaeq1, kas1, exs,
-                  exm, exb, dt_p, cfg, kp, 1);
-        seed_out = 1;
-      }
-      for (int j = 0; j < L; ++j) {
-        lxs[j] = exs[j];
-        lxm[j] = exm[j];
-        lxb[j] = exb[j];
-      }
+      if (failed) break;
     }
     for (int64_t j = 0; j < w; ++j) {
       int64_t i = base + j;
@@ -434,6 +565,8 @@ int64_t oracle_run_range(const ti64_fields* f, int64_t start, int64_t stop,
       f->x_beta[i] = lxb[j];
       f->temperature_old[i] = lt1[j];
     }
+    if (record_iters && !explicit_ && iters_out)
+      for (int64_t j = 0; j < w; ++j) iters_out[base + j] = (int64_t)itc[j];
     if (seed_out)
       for (int64_t j = 0; j < w; ++j) {
         int64_t i = base + j;
@@ -441,8 +574,16 @@ int64_t oracle_run_range(const ti64_fields* f, int64_t start, int64_t stop,
         f->seed_active[i] = lac[j];
         f->seed_direction[i] = ldr[j];
       }
+    if (failed) return base + 1;
   }
   return 0;
+}
+
+/* explicit-scheme entry kept for the existing callers */
+int64_t oracle_run_range(const ti64_fields* f, int64_t start, int64_t stop,
+                         int64_t lanes, int64_t nsub, double dt_sub,
+                         const ti64_kparams* kp, const ti64_icfg* cfg) {
+  return oracle_run_range2(f, start, stop, lanes, nsub, dt_sub, kp, cfg, 0, NULL);
 }
 
 /* batch.py:750-755 _num_substeps */

@@ -154,6 +154,91 @@ def make_steps():
     np.savez_compressed(OUT / "steps.npz", **cases)
 
 
+def make_cn():
+    """Crank-Nicolson step_all cases (batch.py:357-416, halving :568-674)."""
+    from ti64micro.batch import BatchConvergenceError
+    CFG_I = IntegratorConfig(scheme="crank_nicolson")
+    cases = {}
+
+    def add(name, f, dt, lanes, cfg, nsteps=1, vary=None):
+        d = fields_dict(f, "in_")
+        g = f.copy()
+        fail = np.array([], np.int64)
+        iters = None
+        for s in range(nsteps):
+            if vary is not None:
+                g.temperature_new[:] = vary(s)
+            try:
+                iters = step_all(g, dt, DEFAULT_PARAMS, cfg, n_lanes=lanes, record_iters=True)
+            except BatchConvergenceError as e:
+                fail = np.array(e.indices, np.int64)
+                break
+        d.update(fields_dict(g, "out_"))
+        d["dt"] = np.float64(dt)
+        d["lanes"] = np.int64(lanes)
+        d["nsteps"] = np.int64(nsteps)
+        d["fail"] = fail
+        d["iters"] = np.zeros(0, np.int64) if iters is None else np.asarray(iters, np.int64)
+        d["cfg"] = np.array([cfg.dt_sub_max, cfg.eps_abs, cfg.eps_rel,
+                             cfg.max_fixed_point_iters, cfg.initiation_threshold,
+                             cfg.stuck_tol, cfg.max_halvings], np.float64)
+        if vary is not None:
+            d["t_seq"] = np.stack([vary(s) for s in range(nsteps)])
+        for k, v in d.items():
+            cases[f"{name}/{k}"] = v
+
+    for lanes in (1, 2, 4, 8):
+        add(f"cn_random257_l{lanes}", random_states(257, seed=4), 0.01, lanes, CFG_I)
+    add("cn_tail13_l8", random_states(13, seed=6), 0.01, 8, CFG_I)
+    add("cn_sub_dt0.05", random_states(32, seed=12), 0.05, 8, CFG_I)
+    add("cn_sub_dt1.0", random_states(64, seed=15), 1.0, 4, CFG_I)
+    tight = IntegratorConfig(scheme="crank_nicolson", eps_abs=1e-18, eps_rel=1e-8)
+    for lanes in (1, 8):
+        add(f"cn_tight_l{lanes}", random_states(257, seed=5), 0.1, lanes, tight)
+        add(f"cn_tight_dt2e-5_l{lanes}", random_states(257, seed=7), 2e-5, lanes, tight)
+    few = IntegratorConfig(scheme="crank_nicolson", max_fixed_point_iters=3, max_halvings=2,
+                           eps_abs=1e-16, eps_rel=1e-9)
+    for lanes in (1, 4, 8):
+        add(f"cn_halving_l{lanes}", random_states(120, seed=19, t_lo=800.0, t_hi=1300.0),
+            0.01, lanes, few)
+    halv = IntegratorConfig(scheme="crank_nicolson", eps_abs=1e-18, eps_rel=1e-8,
+                            max_fixed_point_iters=6, max_halvings=5, dt_sub_max=1.0)
+    for lanes in (1, 2, 8):
+        add(f"cn_halving2_l{lanes}", random_states(96, seed=23), 0.3, lanes, halv)
+    halv_fail = IntegratorConfig(scheme="crank_nicolson", eps_abs=1e-18, eps_rel=1e-8,
+                                 max_fixed_point_iters=6, max_halvings=1, dt_sub_max=1.0)
+    for lanes in (1, 8):
+        add(f"cn_halving_fail_l{lanes}", random_states(96, seed=23), 0.3, lanes, halv_fail)
+    bad = IntegratorConfig(scheme="crank_nicolson", max_fixed_point_iters=1, max_halvings=0,
+                           dt_sub_max=1.0)
+    add("cn_fail_l8", random_states(40, seed=10, t_lo=950.0, t_hi=1100.0, dt_jitter=0.0),
+        1.0, 8, bad)
+    for lanes in (1, 8):
+        sf = seeding_fields()
+        base_t0 = sf.temperature_old.copy()
+        add(f"cn_seed_40step_l{lanes}", sf, 1e-3, lanes, CFG_I, nsteps=40,
+            vary=lambda s, b=base_t0: b + 3.0 * np.sin(0.3 * s) * (np.arange(len(b)) % 3))
+    add("cn_layout_b10", generate_layout(10, 4096, seed=10), 0.01, 8, CFG_I)
+    np.savez_compressed(OUT / "cn_steps.npz", **cases)
+    hist = {}
+    rng = np.random.default_rng(44)
+    for h in range(4):
+        knots_t = np.concatenate([[0.0], np.sort(rng.uniform(0.1, 6.0, 5))])
+        knots_T = rng.uniform(293.0, 2000.0, 6)
+        times = np.linspace(0.0, knots_t[-1], 1500 if h % 2 == 0 else 60)
+        temps = np.interp(times, knots_t, knots_T)
+        hist[f"h{h}/times"] = times
+        hist[f"h{h}/temps"] = temps
+        hist[f"h{h}/out"] = integrate_history(times, temps, config=CFG_I)
+    times = np.arange(0.0, 400.0, 1.0)
+    hist["const1000/times"] = times
+    hist["const1000/temps"] = np.full_like(times, 1000.0)
+    from ti64micro.kinetics import PhaseState
+    hist["const1000/out"] = integrate_history(times, hist["const1000/temps"],
+                                              state0=PhaseState(0.0, 0.0, 1.0), config=CFG_I)
+    np.savez_compressed(OUT / "cn_history.npz", **hist)
+
+
 def argmax3(xs, xm, xb):
     return np.where((xs >= xm) & (xs >= xb), 0, np.where(xm >= xb, 1, 2))
 
@@ -275,6 +360,12 @@ def make_stencil():
 
 
 if __name__ == "__main__":
+    if "--cn-only" in sys.argv:
+        make_cn()
+        print("cn done")
+        sys.exit(0)
+    make_cn()
+    print("cn done")
     make_fastmath()
     print("fastmath done")
     make_steps()

@@ -117,3 +117,46 @@ def test_stencil_built_sequence_bitwise():
         orc.stencil_step(t, dst, rc, state, DEFAULT_THERMAL.kernel_tuple(), a)
         assert_bitwise(dst, seq[k], f"built step {k}")
         t = dst
+
+
+CN = golden_cases(load_golden("cn_steps.npz"))
+
+
+def _cn_cfg(case):
+    c = case["cfg"]
+    return IntegratorConfig(scheme="crank_nicolson", dt_sub_max=float(c[0]),
+                            eps_abs=float(c[1]), eps_rel=float(c[2]),
+                            max_fixed_point_iters=int(c[3]), initiation_threshold=float(c[4]),
+                            stuck_tol=float(c[5]), max_halvings=int(c[6]))
+
+
+@pytest.mark.parametrize("name", sorted(CN))
+def test_cn_cases_bitwise(name):
+    """Crank-Nicolson + halving (batch.py:357-416, :568-674), lane coupling included."""
+    case = CN[name]
+    cfg = _cn_cfg(case)
+    f = _fields(case, "in_")
+    lanes = int(case["lanes"])
+    dt = float(case["dt"])
+    nsub = orc.num_substeps(dt, cfg.dt_sub_max)
+    fail = []
+    iters = None
+    for s in range(int(case["nsteps"])):
+        if "t_seq" in case:
+            f.temperature_new[:] = case["t_seq"][s]
+        rc, iters = orc.run_range_cn(f, KP, cfg.kernel_tuple(), lanes, nsub, dt / nsub)
+        if rc != 0:
+            fail = list(range(rc - 1, min(rc - 1 + lanes, f.n_points)))
+            break
+    assert fail == list(case["fail"])
+    for k in FIELD_NAMES:
+        assert_bitwise(getattr(f, k), case["out_" + k], f"{name}:{k}")
+    if case["iters"].size and not fail:
+        assert np.array_equal(iters, case["iters"])
+
+
+def test_cn_history_bitwise():
+    for name, case in golden_cases(load_golden("cn_history.npz")).items():
+        cfg = IntegratorConfig(scheme="crank_nicolson").kernel_tuple()
+        out = orc.history(case["times"], case["temps"], case["out"][0], KP, cfg)
+        assert_bitwise(out, case["out"], name)
