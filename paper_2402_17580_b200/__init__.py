@@ -1,5 +1,5 @@
 """paper_2402_17580_b200 — B200-native (sm_100a) per-point Ti-6Al-4V
-microstructure update: a drop-in for ti64micro's explicit ``step_all`` path
+microstructure update: a drop-in for ti64micro's ``step_all`` path (explicit and Crank-Nicolson)
 (reference: ti64micro/__init__.py:11-41 exports).
 
 Importing needs no GPU; every compute call runs in libti64b200.so on an
@@ -9,12 +9,14 @@ sm_100 device and raises ``Ti64Unavailable`` otherwise (no CPU fallback).
 __version__ = "0.1.0"
 
 from .kinetics import DEFAULT_PARAMS, KineticsParams, PhaseState, X_ALPHA_MAX
+from .errors import FixedPointDivergence
 from .integrator import (
     IntegratorConfig,
     SeedingState,
     integrate_history,
     integrate_interval,
     step_crank_nicolson,
+    wrms_norm,
     step_explicit,
 )
 from .batch import (
@@ -41,6 +43,7 @@ __all__ = [
     "KineticsParams", "PhaseState", "DEFAULT_PARAMS", "X_ALPHA_MAX",
     "IntegratorConfig", "SeedingState",
     "step_explicit", "step_crank_nicolson", "integrate_interval", "integrate_history",
+    "FixedPointDivergence", "wrms_norm",
     "GlobalFields", "step_all", "BatchConvergenceError", "SUPPORTED_LANES", "BYTES_PER_POINT",
     "advance", "AdvanceResult", "EventCounters", "phase_sums", "histogram",
     "init_from_source",

@@ -12,7 +12,8 @@ Deviations from the reference API, all deliberate:
     ``host(name)`` return numpy copies;
   * ``threads`` is accepted and ignored (the device decides parallelism);
     results are thread-count invariant exactly as in the reference;
-  * the Crank-Nicolson scheme raises NotImplementedError (explicit only).
+  * on an implicit-scheme failure the points of later batches are left
+    untouched, as in the reference's single sweep (threads=1).
 Additions: ``advance`` (fused multi-step update with on-device temperature
 generators), ``phase_sums``, ``histogram``, ``run_history``.
 """
@@ -23,6 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _abi, _lib
+from .errors import BatchConvergenceError
 from .integrator import IntegratorConfig, num_substeps
 from .kinetics import DEFAULT_PARAMS
 
@@ -39,15 +41,6 @@ _F64 = ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old", "temperature_new"
         "seed_tracked")
 _U8 = ("seed_active", "seed_direction")
 NAMES = _F64[:5] + ("seed_tracked", "seed_active", "seed_direction")
-
-
-class BatchConvergenceError(RuntimeError):
-    """Implicit fixed-point iteration failed (batch.py:74-79)."""
-
-    def __init__(self, indices, message=None):
-        self.indices = list(indices)
-        super().__init__(message or
-                         f"fixed-point iteration failed at point indices {self.indices}")
 
 
 def _torch():
@@ -173,27 +166,33 @@ def step_all(fields, dt, params=DEFAULT_PARAMS, config=IntegratorConfig(), n_lan
              threads=1, record_iters=False, stream=None):
     """Advance every point by the macro step dt (batch.py:762-813).
 
-    Bit-identical to the reference's explicit step_all for the same n_lanes
-    (all eight arrays, including the lane-batch seed write-back).
-    temperature_old takes temperature_new's value in the same pass.
-    Stream-ordered: returns once the kernel is queued on the current stream.
+    Bit-identical to the reference's step_all for the same n_lanes, for both
+    schemes (all eight arrays, including the lane-batch seed write-back and,
+    for Crank-Nicolson, the lane coupling of the batch fixed-point loop and
+    its halving retries).  temperature_old takes temperature_new's value in
+    the same pass.  The explicit scheme is stream-ordered (returns once
+    queued); the implicit scheme synchronises to learn the failing batch.
+
+    Returns the per-point fixed-point iteration counts (int64 CUDA tensor,
+    zero for the explicit scheme) when record_iters is set, else None.
+    Raises BatchConvergenceError naming the first failing batch's points.
     """
     if n_lanes not in SUPPORTED_LANES:
         raise ValueError(f"n_lanes must be one of {SUPPORTED_LANES}")
     if dt <= 0:
         raise ValueError("dt must be positive")
-    if config.scheme != "explicit":
-        raise NotImplementedError(
-            "Crank-Nicolson is not implemented on the B200 path (explicit scheme only)")
     n = fields.n_points
     nsub = num_substeps(float(dt), config.dt_sub_max)
     iters = None
     if record_iters:
         iters = _torch().zeros(n, dtype=_torch().int64, device=fields.device)
-    run_range(fields, 0, n, n_lanes, nsub, float(dt) / nsub, params.kernel_tuple(),
-              config.kernel_tuple(), record_iters, iters, stream)
+    rc = run_range(fields, 0, n, n_lanes, nsub, float(dt) / nsub, params.kernel_tuple(),
+                   config.kernel_tuple(), record_iters, iters, stream)
     fields.traffic_bytes += BYTES_PER_POINT * n
     fields.steps_taken += 1
+    if rc > 0:
+        b = rc - 1
+        raise BatchConvergenceError(list(range(b, min(b + n_lanes, n))))
     return iters
 
 
@@ -277,7 +276,8 @@ def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
     if n_steps < 0 or step0 < 0:
         raise ValueError("n_steps and step0 must be non-negative")
     if config.scheme != "explicit":
-        raise NotImplementedError("Crank-Nicolson is not implemented on the B200 path")
+        return _advance_implicit(fields, n_steps, source, step0, params, config, n_lanes,
+                                 snapshot_every, counters, point_offset, stream)
     lib = _lib.require()
     torch = _torch()
     n = fields.n_points
@@ -318,6 +318,42 @@ def init_from_source(source, n, point_offset=0, device=None):
     f.temperature_new.copy_(f.temperature_old)
     del beam, torch
     return f
+
+
+def _advance_implicit(fields, n_steps, source, step0, params, config, n_lanes,
+                      snapshot_every, counters, point_offset, stream):
+    """advance() for the Crank-Nicolson scheme: the literal loop of its
+    docstring (K3 generator into temperature_new, then the implicit K1), two
+    launches per step plus the snapshot sums.  The implicit step cannot be
+    fused across steps the way K2 fuses the explicit one: a failing batch
+    must stop the sweep (BatchConvergenceError) before the next step runs."""
+    if counters is not None:
+        raise ValueError("event counters are only maintained by the fused explicit advance")
+    lib = _lib.require()
+    torch = _torch()
+    n = fields.n_points
+    dev = fields.device
+    g, beam = tempgen_for(source, point_offset, step0 + n_steps + 1, dev)
+    chunk = snapshot_every if snapshot_every > 0 else max(n_steps, 1)
+    n_snap = (n_steps + chunk - 1) // chunk if n_steps > 0 else 0
+    sums = torch.zeros((max(n_snap, 1), 3), dtype=torch.float64, device=dev)
+    scratch = _scratch(n, dev)
+    launches = 0
+    for k in range(n_steps):
+        _lib.check(lib.ti64_gen_temperature(C.byref(g), n, int(step0 + k + 1),
+                                            _lib.ptr(fields.temperature_new),
+                                            _lib.stream_handle(stream)), "ti64_gen_temperature")
+        step_all(fields, source.dt, params, config, n_lanes, stream=stream)
+        launches += 2
+        if (k + 1) % chunk == 0 or k == n_steps - 1:
+            snap = k // chunk
+            _lib.check(lib.ti64_phase_sums(_lib.ptr(fields.x_alpha_s),
+                                           _lib.ptr(fields.x_alpha_m), _lib.ptr(fields.x_beta),
+                                           n, _lib.ptr(sums[snap]), _lib.ptr(scratch),
+                                           _lib.stream_handle(stream)), "ti64_phase_sums")
+            launches += 2
+    del beam
+    return AdvanceResult(sums=sums, counters=None, steps=n_steps, launches=launches)
 
 
 def gen_temperature(source, n, step, point_offset=0, device=None):

@@ -71,10 +71,14 @@ def test_error_path_without_device():
     assert b"bad argument" in lib.ti64_last_error()
     f = _abi.Fields()
     kp = _abi.KParams()
-    cfg = _abi.ICfg(scheme=1)
+    cfg = _abi.ICfg(scheme=7)
     rc = lib.ti64_run_range(C.byref(f), 0, 10, 8, 1, 1e-5, C.byref(kp), C.byref(cfg), 0,
                             None, None)
-    assert rc == -2
+    assert rc == -1 and b"unknown scheme" in lib.ti64_last_error()
+    cfg = _abi.ICfg(scheme=1, max_halvings=63)
+    rc = lib.ti64_run_range(C.byref(f), 0, 10, 8, 1, 1e-5, C.byref(kp), C.byref(cfg), 0,
+                            None, None)
+    assert rc == -1
     cfg = _abi.ICfg(scheme=0)
     rc = lib.ti64_run_range(C.byref(f), 0, 10, 3, 1, 1e-5, C.byref(kp), C.byref(cfg), 0,
                             None, None)

@@ -96,8 +96,8 @@ def test_validation_errors(pkg):
         pkg.step_all(f, 2e-5, n_lanes=3)
     with pytest.raises(ValueError):
         pkg.step_all(f, -1.0)
-    with pytest.raises(NotImplementedError):
-        pkg.step_all(f, 2e-5, config=pkg.IntegratorConfig(scheme="crank_nicolson"))
+    with pytest.raises(ValueError):
+        pkg.step_all(f, 2e-5, n_lanes=16, config=pkg.IntegratorConfig(scheme="crank_nicolson"))
 
 
 def test_scalar_api_matches_batch(pkg):

@@ -44,8 +44,20 @@ def test_step_all_validates_before_touching_the_device():
         pkg.step_all(_Dummy(), 2e-5, n_lanes=3)
     with pytest.raises(ValueError):
         pkg.step_all(_Dummy(), 0.0)
-    with pytest.raises(NotImplementedError):
-        pkg.step_all(_Dummy(), 1e-5, config=pkg.IntegratorConfig(scheme="crank_nicolson"))
+    with pytest.raises(ValueError):
+        pkg.step_all(_Dummy(), 1e-5, n_lanes=5,
+                     config=pkg.IntegratorConfig(scheme="crank_nicolson"))
+
+
+def test_convergence_error_types_and_wrms():
+    # integrator.py:119-136
+    e = pkg.FixedPointDivergence(pkg.PhaseState(0.1, 0.2, 0.7), 3.5, 50)
+    assert isinstance(e, pkg.BatchConvergenceError) and e.indices == [0]
+    assert e.iters == 50 and e.residual_norm == 3.5
+    cfg = pkg.IntegratorConfig()
+    r, ref = np.array([1e-6, -2e-6]), np.array([0.3, 0.0])
+    w = 1.0 / (cfg.eps_abs + np.abs(ref) * cfg.eps_rel)
+    assert pkg.wrms_norm(r, ref, cfg) == float(np.mean((r * w) ** 2))
 
 
 def test_global_fields_shape_validation():
