@@ -117,6 +117,69 @@ def flops_from_totals(t):
         F_DIS * t["n_dissolve"]
 
 
+# The reference's analytic flop count of one step_all on a layout
+# (bench.py:158-205 count_flops, its per-branch constants bench.py:45-59):
+# a branch any lane of a batch needs is charged to all lanes of the batch;
+# the implicit scheme adds (1 + mean iterations) x the per-iteration work.
+R_EXP, R_LN = 19, 26
+R_POW = R_LN + R_EXP + 1
+R_TFUNCS = 2 + 1 + (R_EXP + 3) + (R_EXP + 4)
+R_XMEQ = R_EXP + 3
+R_SHARED, R_GROW, R_AM, R_DIS = R_POW, R_POW + 3, R_POW + 3, 2 * R_POW + 6
+R_RATES, R_EULER, R_CORR, R_WRMS = 4, 4, 10, 12
+
+
+def reference_flops(xs, xm, t0, t1, n_lanes, scheme="explicit", mean_iters=None,
+                    params=None):
+    from paper_2402_17580_b200.kinetics import DEFAULT_PARAMS
+    p = params or DEFAULT_PARAMS
+    n = len(xs)
+    nbat = (n + n_lanes - 1) // n_lanes
+    pad = nbat * n_lanes
+
+    def batched(a, fill):
+        out = np.full(pad, fill)
+        out[:n] = a
+        out[n:] = a[-1] if n else fill
+        return out.reshape(nbat, n_lanes)
+
+    xs, xm = batched(xs, 0.0), batched(xm, 0.0)
+    t0, t1 = batched(t0, 1000.0), batched(t1, 1000.0)
+    xa = xs + xm
+    fl = 2 * R_TFUNCS * pad
+    fl += R_XMEQ * n_lanes * int((t1 < p.t_alpha_m_start).any(axis=1).sum())
+    # x_alpha_eq(T_old) with numpy exp: only the branch masks depend on it
+    ramp = 1.0 - np.exp(-p.k_alpha_eq * (p.t_alpha_s_start - t0))
+    xaeq0 = np.where(t0 < p.t_alpha_s_end, 0.9, np.where(t0 > p.t_alpha_s_start, 0.0, ramp))
+    grow = (xa < xaeq0) & (xs > 0.0)
+    am = (xm > 0.0) & (xs > 0.0)
+    dis = (xa > xaeq0) & (xa < 0.9)
+    fl += R_SHARED * n_lanes * int((grow.any(axis=1) | am.any(axis=1)).sum())
+    fl += R_GROW * n_lanes * int(grow.any(axis=1).sum())
+    fl += R_AM * n_lanes * int(am.any(axis=1).sum())
+    fl += R_DIS * n_lanes * int(dis.any(axis=1).sum())
+    fl += (R_RATES + R_EULER + R_CORR) * pad
+    if scheme == "crank_nicolson":
+        mi = 2.0 if mean_iters is None else float(mean_iters)
+        per_iter = R_SHARED + R_GROW + R_DIS + R_RATES + R_CORR + R_WRMS
+        fl += int((1.0 + mi) * per_iter * pad)
+    return fl
+
+
+def branch_layout(block, n, seed=0):
+    """The reference's CPU-benchmark layout (bench.py:62-80 generate_layout):
+    alternating blocks of cooling mid-transformation points (beta -> alpha_s
+    growth, ~1000 K) and heating points above equilibrium (alpha_s
+    dissolution, ~1150 K).  numpy's seeded generator, as there."""
+    rng = np.random.default_rng(seed)
+    odd = (np.arange(n) // block) % 2 == 1
+    t_old = np.where(odd, 1150.0, 1000.0) + rng.uniform(-20.0, 20.0, n)
+    t_new = t_old + np.where(odd, 1.0, -1.0)
+    xs = np.where(odd, 0.80, 0.20) + rng.uniform(-0.02, 0.02, n)
+    xm = np.zeros(n)
+    return xs, xm, 1.0 - xs - xm, t_old, t_new
+
+
 # ---------------------------------------------------------------------------
 # CPU reference arm / cpu_baseline: the C oracle (port of the reference
 # algorithm) on the box's host cores.
