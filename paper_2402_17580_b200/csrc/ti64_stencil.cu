@@ -245,7 +245,8 @@ __device__ __forceinline__ void cell_kinetics(ti64_fields& f, uint32_t* __restri
 template <bool COUPLED>
 __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
     const double* __restrict__ src, double* __restrict__ dst, ti64_stencil_args a,
-    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle, CoupledODE o) {
+    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle,
+    const __grid_constant__ CoupledODE o) {
   constexpr int W = TX + 2;              // smem row pitch
   constexpr int SLOT = (TYT + 2) * W;    // doubles per ring slot
   __shared__ double ring[RING * SLOT];
@@ -415,7 +416,8 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, uint64_t desc, int c0,
 template <bool COUPLED>
 __global__ void __launch_bounds__(TX* TY) built_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, double* __restrict__ dst, ti64_stencil_args a,
-    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle, CoupledODE o) {
+    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle,
+    const __grid_constant__ CoupledODE o) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);  // RING slots of SLOT_BYTES
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT_BYTES);
