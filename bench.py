@@ -320,6 +320,29 @@ def measure_extra(torch, pkg, dev):
         t = _time_dev(torch, lambda: pkg.advance(f.copy(), 2000, src_c, step0=200,
                                                 snapshot_every=1000), 1)
         out[f"config{c}_shard_2^22x2000"] = {"point_updates_per_s": (1 << 22) * 2000 / t}
+    # Crank-Nicolson step_all on the reference's block-100 benchmark layout
+    # (bench.py:131-155: dt = dt_sub_max = 0.01), its analytic flop count
+    cfg = pkg.IntegratorConfig(scheme="crank_nicolson", dt_sub_max=0.01)
+    n = 1 << 22
+    lay = branch_layout(100, n)
+    pristine = pkg.GlobalFields(*lay, device=dev)
+    it = pkg.step_all(pristine.copy(), 0.01, config=cfg, n_lanes=8, record_iters=True)
+    mean_it = it.double().mean().item()
+    work = [pristine.copy() for _ in range(5)]
+    ts = []
+    for w in work:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pkg.step_all(w, 0.01, config=cfg, n_lanes=8)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    t = sorted(ts)[len(ts) // 2]
+    fl = reference_flops(lay[0], lay[1], lay[3], lay[4], 8, "crank_nicolson", mean_it)
+    out["crank_nicolson_layout_block100_2^22"] = {
+        "point_updates_per_s": n / t, "GDoF_per_s": 3 * n / t / 1e9, "ms": t * 1e3,
+        "mean_fixed_point_iters": mean_it, "reference_flops_per_point": fl / n,
+        "TFLOP/s": fl / t / 1e12, "note": "includes the per-call failure readback (sync)"}
     return out
 
 
@@ -428,6 +451,9 @@ def run_b200(args):
         flops_launch = flops_job / (nsteps // SNAP_EVERY)
         achieved = flops_launch / per_launch_s / 1e12
         peak_tf = peak / 1e12
+        cn = (extra or {}).get("crank_nicolson_layout_block100_2^22")
+        if cn:
+            cn["frac_of_fp64_peak"] = cn["TFLOP/s"] / peak_tf
         cpu = None if args.no_cpu_baseline else cpu_reference(budget_s=args.cpu_budget)
         clocks = clk.summary()
         line = {
