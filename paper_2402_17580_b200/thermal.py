@@ -1,10 +1,16 @@
-"""Heat-equation stencil path (config 3) — parameters and field container.
+"""Heat-equation stencil path and the coupled layer build, on the GPU.
 
-Mirrors the subset of ti64micro/thermal.py that the coupled config needs:
-``ThermalParams`` / ``kernel_tuple`` (thermal.py:50-104), ``HeatSource``
-(thermal.py:107-121), ``stable_dt`` (thermal.py:168-170), ``ThermalField``
-(thermal.py:177-202) and ``step_thermal`` (thermal.py:321-354), the latter
-running the K4 kernel (csrc/ti64_stencil.cu) on device-resident grids.
+Mirrors ti64micro/thermal.py: ``ThermalParams`` / ``kernel_tuple``
+(thermal.py:50-104), ``HeatSource`` (:107-121), the point-wise helpers
+``conductivity`` / ``update_consolidation`` / ``source_term`` /
+``surface_losses`` (:124-165), ``stable_dt`` (:168-170), ``ThermalField``
+(:177-202), ``step_thermal`` (:321-354, the K4 kernels of
+csrc/ti64_stencil.cu on device-resident grids), and the build driver
+``BuildGeometry`` / ``BuildSchedule`` / ``allocate_domain`` /
+``activate_layer`` / ``run_build`` (:362-589), whose every thermal and
+kinetics step runs on the device (step_thermal + step_all on the active
+z-prefix, exactly the reference's ``couple``).  ``CoupledDomain`` is the
+all-built config-3 block with the fused stencil+kinetics kernel.
 """
 
 import math
@@ -12,7 +18,11 @@ from dataclasses import dataclass, replace
 from typing import NamedTuple
 
 __all__ = ["KernelThermalParams", "ThermalParams", "DEFAULT_THERMAL", "HeatSource",
-           "stable_dt", "STATE_INACTIVE", "STATE_POWDER", "STATE_BUILT", "SIGMA_S"]
+           "stable_dt", "STATE_INACTIVE", "STATE_POWDER", "STATE_BUILT", "SIGMA_S",
+           "conductivity", "update_consolidation", "source_term", "surface_losses",
+           "ThermalField", "step_thermal", "CoupledDomain", "BuildGeometry",
+           "BuildSchedule", "allocate_domain", "activate_layer", "cooldown_steps",
+           "run_build"]
 
 STATE_INACTIVE = 0
 STATE_POWDER = 1
@@ -102,6 +112,52 @@ def stable_dt(h, params=DEFAULT_THERMAL):
     return h * h * params.rho * params.c / (6.0 * params.k_ms)
 
 
+def _np(a):
+    import numpy as np
+    return np.asarray(a, dtype=np.float64)
+
+
+def _ret(out):
+    return float(out) if out.ndim == 0 else out
+
+
+def conductivity(t, r_c, params=DEFAULT_THERMAL):
+    """r_p k_p + r_m k_m + r_s k_s with k_m = k_s (thermal.py:124-133)."""
+    import numpy as np
+    t, r_c = _np(t), _np(r_c)
+    g = np.clip((t - params.t_sol) / (params.t_liq - params.t_sol), 0.0, 1.0)
+    return _ret((1.0 - r_c) * params.k_p + g * params.k_ms + (r_c - g) * params.k_ms)
+
+
+def update_consolidation(r_c, t, powder_origin, params=DEFAULT_THERMAL):
+    """Running max of the liquid fraction for powder voxels (thermal.py:136-139)."""
+    import numpy as np
+    g = np.clip((_np(t) - params.t_sol) / (params.t_liq - params.t_sol), 0.0, 1.0)
+    return np.where(powder_origin, np.maximum(r_c, g), r_c)
+
+
+def source_term(x, y, z_below_surface, beam_x, beam_y, source=HeatSource(), params=None):
+    """Volumetric beam input at a point (thermal.py:142-148); the exponential
+    is the device fast_exp."""
+    import numpy as np
+    from .batch import fast_exp
+    r2 = (_np(x) - beam_x) ** 2 + (_np(y) - beam_y) ** 2
+    q = source.peak * _np(fast_exp(-2.0 * r2 / source.radius**2))
+    return _ret(np.where(_np(z_below_surface) < source.h_powder, q, 0.0))
+
+
+def surface_losses(t, params=DEFAULT_THERMAL):
+    """Radiative + evaporative flux of exposed top faces (thermal.py:151-165)."""
+    import numpy as np
+    from .batch import fast_exp
+    t = _np(t)
+    q_rad = params.emissivity * params.sigma_s * (t**4 - params.t_inf**4)
+    tc = np.minimum(t, params.t_max_clamp)
+    q_evap = (0.82 * params.c_p * _np(fast_exp(-params.c_t * (1.0 / tc - 1.0 / params.t_v)))
+              * np.sqrt(params.c_m / tc) * (params.h_v + params.c * (tc - params.t_h0)))
+    return _ret(q_rad + np.where(tc > params.t_v, q_evap, 0.0))
+
+
 # --------------------------------------------------------------------------
 # device-resident field and the K4 step (thermal.py:177-202, :321-354)
 # --------------------------------------------------------------------------
@@ -128,6 +184,18 @@ class ThermalField:
         """True when every cell is STATE_BUILT with r_c == 1 (config 3)."""
         return bool((self.state == STATE_BUILT).all().item() and
                     (self.r_c == 1.0).all().item())
+
+    def active_mask(self):
+        return self.state != STATE_INACTIVE
+
+    def enthalpy(self, params=DEFAULT_THERMAL):
+        """Total rho c T h^3 over active voxels (thermal.py:193-196)."""
+        m = self.active_mask()
+        return float(params.rho * params.c * self.h**3 * self.temperature_old[m].sum().item())
+
+    def commit_temperatures(self):
+        """Adopt temperature_new as current (thermal.py:198-200)."""
+        self.temperature_old.copy_(self.temperature_new)
 
 
 def step_thermal(field, dt, params=DEFAULT_THERMAL, source=None, beam=None, losses=True,
@@ -260,3 +328,256 @@ class CoupledDomain:
         self.fields.traffic_bytes += 72 * self.fields.n_points * n_steps
         self.fields.steps_taken += n_steps
         return self
+
+
+# --------------------------------------------------------------------------
+# layer build (thermal.py:362-589)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class BuildGeometry:
+    """Axis-aligned box part centred on a box base plate, SI units
+    (thermal.py:362-403)."""
+
+    plate_size: tuple = (1.2e-3, 1.2e-3, 0.2e-3)
+    part_size: tuple = (1.0e-3, 1.0e-3, 0.25e-3)
+    voxel: float = 0.05e-3
+
+    def __post_init__(self):
+        if self.voxel <= 0:
+            raise ValueError("voxel size must be positive")
+        for a, b in zip(self.part_size[:2], self.plate_size[:2]):
+            if a > b + 1e-12:
+                raise ValueError("part footprint must fit on the plate")
+
+    @property
+    def grid(self):
+        h = self.voxel
+        return (int(round(self.plate_size[0] / h)), int(round(self.plate_size[1] / h)),
+                int(round(self.plate_size[2] / h)), int(round(self.part_size[2] / h)))
+
+    @property
+    def part_box(self):
+        nx, ny, _, _ = self.grid
+        h = self.voxel
+        px = int(round(self.part_size[0] / h))
+        py = int(round(self.part_size[1] / h))
+        ix0, iy0 = (nx - px) // 2, (ny - py) // 2
+        return (ix0, ix0 + px), (iy0, iy0 + py)
+
+    @property
+    def part_extent(self):
+        (ix0, ix1), (iy0, iy1) = self.part_box
+        h = self.voxel
+        return (ix0 * h, iy0 * h, ix1 * h, iy1 * h)
+
+
+@dataclass(frozen=True)
+class BuildSchedule:
+    """Time-stepping schedule of the layer build (thermal.py:406-417)."""
+
+    dt_active: float = 2e-5
+    interlayer_dwell: float = 1.0
+    initial_dwell_steps: int = 2000
+    growth_every: int = 10
+    dt_max: float = 0.1
+    final_cooldown: float = 100.0
+    preheat: float = 293.0
+    room: float = 293.0
+
+
+def _fresh_solid(t, kinetics_params):
+    from .batch import corrected_beta_state
+    xs, xm, xb = corrected_beta_state([float(t)], kinetics_params)
+    return float(xs[0]), float(xm[0]), float(xb[0])
+
+
+def allocate_domain(geometry, schedule, kinetics_params=None, device=None):
+    """Plate active (built, r_c = 1), part inactive; kinetics fields on every
+    voxel with the thermal temperatures as views of theirs; plate
+    microstructure = fresh solid corrected at the preheat (thermal.py:420-438)."""
+    import torch
+    from .batch import GlobalFields
+    from .kinetics import DEFAULT_PARAMS
+    kp = kinetics_params or DEFAULT_PARAMS
+    nx, ny, nz_plate, n_layers = geometry.grid
+    nz = nz_plate + n_layers
+    fields = GlobalFields.allocate(nz * ny * nx, temperature=schedule.preheat, device=device)
+    dev = fields.device
+    state = torch.zeros((nz, ny, nx), dtype=torch.uint8, device=dev)
+    state[:nz_plate] = STATE_BUILT
+    r_c = torch.zeros((nz, ny, nx), dtype=torch.float64, device=dev)
+    r_c[:nz_plate] = 1.0
+    field = ThermalField(fields.temperature_old.view(nz, ny, nx),
+                         fields.temperature_new.view(nz, ny, nx), r_c, state,
+                         geometry.voxel, nz_plate)
+    xs, xm, xb = _fresh_solid(schedule.preheat, kp)
+    fields.x_alpha_s.fill_(xs)
+    fields.x_alpha_m.fill_(xm)
+    fields.x_beta.fill_(xb)
+    return field, fields
+
+
+def activate_layer(field, fields, geometry, schedule, kinetics_params=None):
+    """Next powder layer at the preheat temperature, r_c = 0, fresh solid
+    microstructure; ValueError once the build is complete (thermal.py:441-463)."""
+    from .kinetics import DEFAULT_PARAMS
+    nx, ny, nz_plate, n_layers = geometry.grid
+    if field.z_top >= nz_plate + n_layers:
+        raise ValueError("build complete: no layer left to activate")
+    (ix0, ix1), (iy0, iy1) = geometry.part_box
+    z = field.z_top
+    field.state[z, iy0:iy1, ix0:ix1] = STATE_POWDER
+    field.r_c[z, iy0:iy1, ix0:ix1] = 0.0
+    field.temperature_old[z, iy0:iy1, ix0:ix1] = schedule.preheat
+    field.temperature_new[z, iy0:iy1, ix0:ix1] = schedule.preheat
+    nzz, nyy, nxx = field.shape
+    xs, xm, xb = _fresh_solid(schedule.preheat, kinetics_params or DEFAULT_PARAMS)
+    for arr, v in ((fields.x_alpha_s, xs), (fields.x_alpha_m, xm), (fields.x_beta, xb)):
+        arr.view(nzz, nyy, nxx)[z, iy0:iy1, ix0:ix1] = v
+    field.z_top = z + 1
+    return field
+
+
+def _active_prefix(field, fields):
+    """GlobalFields over the active z-prefix, sharing storage (thermal.py:466-474)."""
+    from .batch import GlobalFields
+    nz, ny, nx = field.shape
+    m = field.z_top * ny * nx
+    return GlobalFields(*[getattr(fields, k)[:m] for k in (
+        "x_alpha_s", "x_alpha_m", "x_beta", "temperature_old", "temperature_new",
+        "seed_tracked", "seed_active", "seed_direction")], device=fields.device)
+
+
+def cooldown_steps(duration, schedule, initial_steps):
+    """Macro step sizes of one cool-down phase: `initial_steps` at dt_active,
+    then doubling every growth_every steps up to dt_max, the last step cut to
+    land on `duration` (thermal.py:477-495)."""
+    steps = []
+    t = 0.0
+    dt = schedule.dt_active
+    count = 0
+    while t < duration - 1e-12:
+        if count > initial_steps and (count - initial_steps) % schedule.growth_every == 0:
+            dt = min(dt * 2.0, schedule.dt_max)
+        dt_eff = min(dt, duration - t)
+        steps.append(dt_eff)
+        t += dt_eff
+        count += 1
+    return steps
+
+
+def run_build(geometry, scan_path, schedule=BuildSchedule(), thermal_params=DEFAULT_THERMAL,
+              kinetics_params=None, integrator_config=None, source=None, n_lanes=8,
+              threads=1, probe_points=(), snapshot_hook=None, probe_hook=None, device=None):
+    """Coupled scan-resolved build (thermal.py:498-589), every step on the GPU.
+
+    Per layer: activate the powder layer, trace the layer's segments at
+    dt_active, then the interlayer cool-down with growing steps; finally a
+    cool-down with the bottom held at room temperature.  Each macro step is
+    the reference's ``couple``: step_thermal (K4, losses on) then step_all
+    on the active z-prefix, which consumes the (T_n, T_n+1) pair in place.
+
+    Returns (field, fields, probes): probes maps probe index -> list of
+    (t, T, x_alpha_s, x_alpha_m, x_beta) rows, gathered on the device every
+    step and copied to the host once at the end; ``probes.timings`` holds
+    the phase wall-clock split (synchronised at phase ends; the device work
+    is asynchronous, so thermal_s / kinetics_s are not split and stay 0).
+    ``threads`` is accepted and ignored.
+    """
+    import math
+    import time as _time
+
+    import torch
+
+    from .batch import step_all
+    from .integrator import IntegratorConfig
+    from .kinetics import DEFAULT_PARAMS
+    from .scanpath import beam_position, beam_timeline
+
+    kp = kinetics_params or DEFAULT_PARAMS
+    cfg = integrator_config or IntegratorConfig(scheme="explicit")
+    source = source or HeatSource(h_powder=geometry.voxel)
+    field, fields = allocate_domain(geometry, schedule, kp, device=device)
+    nx, ny, nz_plate, n_layers = geometry.grid
+    dev = fields.device
+
+    class ProbeSet(dict):
+        timings = None
+
+    probes = ProbeSet({i: [] for i in range(len(probe_points))})
+    probes.timings = {"active_s": 0.0, "cooldown_s": 0.0, "final_s": 0.0,
+                      "thermal_s": 0.0, "kinetics_s": 0.0}
+    pidx = []
+    for (px, py, pz) in probe_points:
+        ix = min(nx - 1, max(0, int(px / geometry.voxel)))
+        iy = min(ny - 1, max(0, int(py / geometry.voxel)))
+        iz = min(nz_plate + n_layers - 1, max(0, int(pz / geometry.voxel)))
+        pidx.append((iz, iy, ix))
+    flat = torch.tensor([(iz * ny + iy) * nx + ix for iz, iy, ix in pidx], dtype=torch.int64,
+                        device=dev)
+    rows = []   # (t_now, probes inside the active prefix, device row (n_probes, 5))
+    t_now = 0.0
+    counts = [0, 0]
+    state_flat = field.state.view(-1)
+
+    def couple(dt, beam, bottom, phase):
+        nonlocal t_now
+        step_thermal(field, dt, thermal_params, source, beam, losses=True,
+                     bottom_dirichlet=bottom, all_built=False)
+        counts[0] += 1
+        step_all(_active_prefix(field, fields), dt, kp, cfg, n_lanes=n_lanes)
+        counts[1] += 1
+        t_now += dt
+        if probe_hook is not None:
+            probe_hook(t_now, field, fields)
+        elif len(pidx):
+            rows.append((t_now, [iz < field.z_top for iz, _, _ in pidx],
+                         torch.stack([state_flat[flat].double(), fields.temperature_old[flat],
+                                      fields.x_alpha_s[flat], fields.x_alpha_m[flat],
+                                      fields.x_beta[flat]], 1)))
+
+    def timed(phase, fn):
+        torch.cuda.synchronize(dev)
+        w0 = _time.perf_counter()
+        fn()
+        torch.cuda.synchronize(dev)
+        probes.timings[phase] += _time.perf_counter() - w0
+
+    for layer in range(n_layers):
+        activate_layer(field, fields, geometry, schedule, kp)
+        segments = scan_path.layer_segments(layer)
+        if segments:
+            spans = beam_timeline(segments)
+            t_active = spans[-1][1]
+            n_steps = max(1, int(math.ceil(t_active / schedule.dt_active - 1e-12)))
+
+            def active():
+                for k in range(n_steps):
+                    tq = min((k + 0.5) * schedule.dt_active, t_active)
+                    couple(schedule.dt_active, beam_position(segments, tq, spans),
+                           schedule.preheat, "active_s")
+            timed("active_s", active)
+
+        def dwell():
+            for dt in cooldown_steps(scan_path.dwell, schedule, schedule.initial_dwell_steps):
+                couple(dt, None, schedule.preheat, "cooldown_s")
+        timed("cooldown_s", dwell)
+        if snapshot_hook is not None:
+            snapshot_hook(f"layer_{layer:04d}", t_now, field, fields)
+
+    def final():
+        for dt in cooldown_steps(schedule.final_cooldown, schedule, 0):
+            couple(dt, None, schedule.room, "final_s")
+    timed("final_s", final)
+    if snapshot_hook is not None:
+        snapshot_hook("final", t_now, field, fields)
+    assert counts[0] == counts[1], "coupling order violated"
+    if rows:
+        vals = torch.stack([r[2] for r in rows]).cpu().numpy()  # one copy for the run
+        for k, (t, live, _) in enumerate(rows):
+            for pi in range(len(pidx)):
+                if live[pi] and vals[k, pi, 0] != STATE_INACTIVE:
+                    probes[pi].append((t, float(vals[k, pi, 1]), float(vals[k, pi, 2]),
+                                       float(vals[k, pi, 3]), float(vals[k, pi, 4])))
+    return field, fields, probes

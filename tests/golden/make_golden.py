@@ -20,6 +20,11 @@ reference's own entry points:
                  reference's step_all; counters per DESIGN.md §3 in numpy
   history.npz    integrate_history (integrator.py:303-325)
   stencil.npz    thermal._stencil_step via step_thermal (thermal.py:321-354)
+  cn_steps.npz, cn_history.npz  Crank-Nicolson step_all / integrate_history
+  build.npz      thermal.run_build on the reference's micro build
+                 (test_thermal.py:33-43, :192-200): final thermal field, all
+                 kinetics arrays, probe rows, for several scan strategies /
+                 schemes / powers
 
 The GPU box never runs this script (no /root/reference there); tests read
 only the committed .npz files.
@@ -359,13 +364,69 @@ def make_stencil():
     np.savez_compressed(OUT / "stencil.npz", **cases)
 
 
+def make_build():
+    """run_build (thermal.py:498-589) on the reference tests' micro geometry."""
+    from ti64micro.scanpath import ScanPath, serpentine, four_islands
+    MM = 1e-3
+    geom = th.BuildGeometry(plate_size=(0.6 * MM, 0.6 * MM, 0.15 * MM),
+                            part_size=(0.4 * MM, 0.4 * MM, 0.1 * MM), voxel=0.05 * MM)
+    cases = {}
+
+    def run(name, power, strategy, cfg=None, **kw):
+        base = dict(dt_active=2e-5, interlayer_dwell=0.02, initial_dwell_steps=50,
+                    final_cooldown=1.0, preheat=293.0)
+        base.update(kw)
+        sched = th.BuildSchedule(**base)
+        segs = []
+        for layer in range(geom.grid[3]):
+            segs.extend(strategy(geom.part_extent, 0.08 * MM, 0.96, power, layer))
+        scan = ScanPath(segs, dwell=sched.interlayer_dwell)
+        field, fields, probes = th.run_build(
+            geom, scan, sched, integrator_config=cfg,
+            probe_points=[(0.3 * MM, 0.3 * MM, 0.17 * MM), (0.1 * MM, 0.2 * MM, 0.05 * MM)])
+        d = {f"{name}/{k}": np.array(getattr(fields, k)) for k in NAMES}
+        d[f"{name}/r_c"] = np.array(field.r_c)
+        d[f"{name}/state"] = np.array(field.state)
+        d[f"{name}/z_top"] = np.int64(field.z_top)
+        for i in range(2):
+            d[f"{name}/probe{i}"] = np.array(probes[i], dtype=np.float64).reshape(-1, 5)
+        d[f"{name}/power"] = np.float64(power)
+        d[f"{name}/strategy"] = np.array(strategy.__name__)
+        d[f"{name}/scheme"] = np.array("explicit" if cfg is None else cfg.scheme)
+        d[f"{name}/sched"] = np.array([sched.dt_active, sched.interlayer_dwell,
+                                       sched.initial_dwell_steps, sched.growth_every,
+                                       sched.dt_max, sched.final_cooldown, sched.preheat,
+                                       sched.room])
+        cases.update(d)
+
+    for dur, init, dtmax in ((0.02, 50, 0.1), (1.0, 0, 0.1), (100.0, 2000, 0.1), (0.3, 7, 0.05)):
+        sc = th.BuildSchedule(dt_max=dtmax)
+        cases[f"cooldown/{dur}_{init}_{dtmax}"] = np.array(th._cooldown_steps(dur, sc, init))
+    g = th.BuildGeometry()
+    cases["geometry/default_grid"] = np.array(g.grid)
+    cases["geometry/default_part_box"] = np.array(g.part_box)
+    cases["geometry/default_part_extent"] = np.array(g.part_extent)
+    run("serp180", 180.0, serpentine)
+    run("islands150", 150.0, four_islands, preheat=400.0)
+    run("zero", 0.0, serpentine)
+    run("serp180_cn", 180.0, serpentine, cfg=IntegratorConfig(scheme="crank_nicolson"),
+        final_cooldown=0.3)
+    np.savez_compressed(OUT / "build.npz", **cases)
+
+
 if __name__ == "__main__":
+    if "--build-only" in sys.argv:
+        make_build()
+        print("build done")
+        sys.exit(0)
     if "--cn-only" in sys.argv:
         make_cn()
         print("cn done")
         sys.exit(0)
     make_cn()
     print("cn done")
+    make_build()
+    print("build done")
     make_fastmath()
     print("fastmath done")
     make_steps()
