@@ -402,6 +402,21 @@ def make_build():
     for dur, init, dtmax in ((0.02, 50, 0.1), (1.0, 0, 0.1), (100.0, 2000, 0.1), (0.3, 7, 0.05)):
         sc = th.BuildSchedule(dt_max=dtmax)
         cases[f"cooldown/{dur}_{init}_{dtmax}"] = np.array(th._cooldown_steps(dur, sc, init))
+    rng = np.random.default_rng(11)
+    t = np.concatenate([rng.uniform(250.0, 5000.0, 200), [1878.0, 1903.0, 1928.0, 3130.0, 4130.0, 4500.0]])
+    rc = rng.uniform(0.0, 1.0, t.size)
+    cases["helpers/t"] = t
+    cases["helpers/rc"] = rc
+    cases["helpers/conductivity"] = th.conductivity(t, rc)
+    powder = rng.uniform(size=t.size) < 0.5
+    cases["helpers/powder"] = powder
+    cases["helpers/update_consolidation"] = th.update_consolidation(rc, t, powder)
+    cases["helpers/surface_losses"] = th.surface_losses(t)
+    x = rng.uniform(0.0, 1e-3, 300)
+    y = rng.uniform(0.0, 1e-3, 300)
+    zb = rng.uniform(0.0, 1e-4, 300)
+    cases["helpers/x"], cases["helpers/y"], cases["helpers/zb"] = x, y, zb
+    cases["helpers/source_term"] = th.source_term(x, y, zb, 4e-4, 5e-4)
     g = th.BuildGeometry()
     cases["geometry/default_grid"] = np.array(g.grid)
     cases["geometry/default_part_box"] = np.array(g.part_box)

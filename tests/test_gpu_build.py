@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 G = load_golden("build.npz")
 CASES = sorted({k.split("/")[0] for k in G.files
-                if k.split("/")[0] not in ("cooldown", "geometry")})
+                if k.split("/")[0] not in ("cooldown", "geometry", "helpers")})
 MM = 1e-3
 
 
@@ -77,3 +77,15 @@ def test_build_physics(pkg):
     _run(pkg, "serp180", snapshot_hook=lambda label, t, f, kf: snaps.append(
         f.r_c.cpu().numpy().copy()))
     assert all(np.all(b >= a - 1e-15) for a, b in zip(snaps, snaps[1:]))
+
+
+def test_pointwise_helpers_match_reference(pkg):
+    """thermal.py:124-165 (the exponentials through the device fast_exp)."""
+    from paper_2402_17580_b200 import thermal as th
+    t, rc = G["helpers/t"], G["helpers/rc"]
+    assert_bitwise(th.conductivity(t, rc), G["helpers/conductivity"], "conductivity")
+    assert_bitwise(th.update_consolidation(rc, t, G["helpers/powder"]),
+                   G["helpers/update_consolidation"], "update_consolidation")
+    assert_bitwise(th.surface_losses(t), G["helpers/surface_losses"], "surface_losses")
+    assert_bitwise(th.source_term(G["helpers/x"], G["helpers/y"], G["helpers/zb"], 4e-4, 5e-4),
+                   G["helpers/source_term"], "source_term")
