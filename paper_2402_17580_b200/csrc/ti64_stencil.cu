@@ -175,14 +175,6 @@ struct CoupledODE {
 constexpr int PD = PD_DEF;           // planes prefetched beyond z+1
 constexpr int RING = PD + 3;    // planes z-1, z, z+1 and PD more
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async4(uint32_t* smem, const uint32_t* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -361,9 +353,27 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
 // the box starts at x0 - 2: TMA needs the innermost start coordinate 16-byte
 // aligned (measured: an odd double offset faults), so 2 halo columns on the
 // left (one unused) and 2 on the right keep the box 36 doubles = 288 B wide
-constexpr int BOX_X = TX + 4, BOX_Y = TYT + 2;
-constexpr int BOX_BYTES = BOX_X * BOX_Y * 8;
-constexpr int SLOT_BYTES = (BOX_BYTES + 127) / 128 * 128;
+constexpr int BOX_X = TX + 4;
+// rows per thread of the TMA kernels: the plain stencil keeps 2 (more resident
+// blocks), the fused coupled step takes 4 (its per-plane kinetics bookkeeping
+// is shared by more cells); measured on the config-3 grid
+#ifndef RY_S_DEF
+#define RY_S_DEF 2
+#endif
+#ifndef RY_C_DEF
+#define RY_C_DEF 4
+#endif
+template <int RYV>
+struct TmaTile {
+  static constexpr int RY = RYV;
+  static constexpr int TYT = TY * RYV;
+  static constexpr int BOX_Y = TYT + 2;
+  static constexpr int BOX_BYTES = BOX_X * BOX_Y * 8;
+  static constexpr int SLOT_BYTES = (BOX_BYTES + 127) / 128 * 128;
+  static constexpr int SMEM = RING * SLOT_BYTES + RING * 8 + RING * TYT * 4;
+};
+template <bool COUPLED>
+using TileOf = TmaTile<COUPLED ? RY_C_DEF : RY_S_DEF>;
 
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -372,30 +382,28 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
                : "memory");
 }
-// bounded wait: a transaction that never lands traps (kernel error) instead
-// of hanging the GPU
+__device__ __forceinline__ unsigned mbar_try(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
+// bounded wait: the common case (data landed, or lands within try_wait's own
+// suspend window) costs one try_wait; the clock is read only after a miss,
+// and a transaction that never lands traps instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  if (mbar_try(bar, parity)) return;
   const long long t0 = clock64();
-  for (;;) {
-    unsigned ok;
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    if (ok) return;
+  while (!mbar_try(bar, parity)) {
     if (clock64() - t0 > 4000000000LL) {  // ~2 s: a transaction never landed
-      unsigned other;
-      asm volatile(
-          "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-          " selp.u32 %0, 1, 0, p;\n}\n"
-          : "=r"(other)
-          : "r"(bar), "r"(parity ^ 1u));
       if (threadIdx.x == 0 && threadIdx.y == 0)
-        printf("ti64 TMA wait timeout: block (%d,%d,%d) bar %u parity %u other-phase-done %u\n",
-               blockIdx.x, blockIdx.y, blockIdx.z, bar, parity, other);
+        printf("ti64 TMA wait timeout: block (%d,%d,%d) bar %u parity %u\n", blockIdx.x,
+               blockIdx.y, blockIdx.z, bar, parity);
 #ifdef TI64_TMA_DEBUG
       return;
 #else
@@ -413,11 +421,19 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, uint64_t desc, int c0,
       : "memory");
 }
 
+#ifndef TMA_MINB
+#define TMA_MINB 4
+#endif
+#ifndef TMA_MINB_C
+#define TMA_MINB_C 1
+#endif
 template <bool COUPLED>
-__global__ void __launch_bounds__(TX* TY) built_tma_kernel(
+__global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, double* __restrict__ dst, ti64_stencil_args a,
     StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle,
     const __grid_constant__ CoupledODE o) {
+  using T = TileOf<COUPLED>;
+  constexpr int RY = T::RY, TYT = T::TYT, BOX_BYTES = T::BOX_BYTES, SLOT_BYTES = T::SLOT_BYTES;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);  // RING slots of SLOT_BYTES
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT_BYTES);
@@ -496,6 +512,8 @@ __global__ void __launch_bounds__(TX* TY) built_tma_kernel(
   const unsigned gm =
       COUPLED ? (((o.L >= 32) ? 0xffffffffu : ((1u << o.L) - 1u)) << (lane & ~(o.L - 1))) : 0u;
   double* dcol = dst + (-a.z_base) * plane + x;
+  // block-uniform: every cell of the tile has all four in-plane neighbours
+  const bool xy_interior = x0 > 0 && x0 + TX < nx && ybase > 0 && ybase + TYT < ny;
 
   for (int z = z0; z < z1; ++z) {
     issue(z + 1 + PD, si);
@@ -503,6 +521,31 @@ __global__ void __launch_bounds__(TX* TY) built_tma_kernel(
     if (COUPLED) {
       cp_async_wait<PD>();
       __syncthreads();
+    }
+    if (!COUPLED && xy_interior && z > 0 && z + 1 < nz &&
+        !(a.source_on != 0 && z == a.z_top - 1)) {
+      // interior plane of an interior tile: all six faces present, no source
+      // or boundary value; same face order and association as below
+      double* dz = dcol + (int64_t)z * plane;
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const double* P = ring + s0 * SLOTD + cidx[r];
+        const double t0 = P[0];
+        double flux = __dadd_rn(0.0, __dmul_rn(kf, __dsub_rn(P[-1], t0)));
+        flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[1], t0)));
+        flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[-W], t0)));
+        flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[W], t0)));
+        flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sm * SLOTD + cidx[r]], t0)));
+        flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sp1 * SLOTD + cidx[r]], t0)));
+        dz[(int64_t)yr[r] * nx] = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
+      }
+      __syncthreads();
+      const int t = sm;
+      sm = s0;
+      s0 = sp1;
+      sp1 = (sp1 + 1 == RING) ? 0 : sp1 + 1;
+      si = t;
+      continue;
     }
     double tm_[RY];
 #pragma unroll
@@ -566,16 +609,17 @@ EncodeTiledFn encoder() {
 }
 
 // 3D map over the stored planes (x fastest); false when TMA cannot be used
-bool make_plane_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t nzs) {
+bool make_plane_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t nzs,
+                    int box_y) {
   EncodeTiledFn enc = encoder();
   // the box must fit inside the tensor (a box wider than the grid stalls)
   if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || (nx * 8) % 16 != 0 || nx < BOX_X ||
-      ny < BOX_Y ||
+      ny < box_y ||
       nx > (1LL << 31) || ny > (1LL << 31) || nzs > (1LL << 31))
     return false;
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nzs};
   cuuint64_t strides[2] = {(cuuint64_t)(nx * 8), (cuuint64_t)(nx * ny * 8)};
-  cuuint32_t box[3] = {(cuuint32_t)BOX_X, (cuuint32_t)BOX_Y, 1u};
+  cuuint32_t box[3] = {(cuuint32_t)BOX_X, (cuuint32_t)box_y, 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   std::memset(m, 0, sizeof(*m));
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
@@ -584,21 +628,24 @@ bool make_plane_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr int TMA_SMEM = RING * SLOT_BYTES + RING * 8 + RING * TYT * 4;
-
+// TMA launch: false when the grid cannot be mapped (callers fall back to the
+// cp.async kernel); the grid's y extent follows the kernel's own tile height
 template <bool COUPLED>
 bool launch_built(const double* src, double* dst, const ti64_stencil_args& a,
                   const StencilConst& c, ti64_fields f, uint32_t* idle, const CoupledODE& o,
-                  dim3 grid, int zchunk, cudaStream_t st) {
+                  int64_t nz_units, int zchunk, cudaStream_t st) {
+  using T = TileOf<COUPLED>;
   CUtensorMap m;
-  if (!make_plane_map(&m, src, a.nx, a.ny, a.nz_stored)) return false;
+  if (!make_plane_map(&m, src, a.nx, a.ny, a.nz_stored, T::BOX_Y)) return false;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(built_tma_kernel<COUPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TMA_SMEM);
+                         T::SMEM);
     attr_set = true;
   }
-  built_tma_kernel<COUPLED><<<grid, dim3(TX, TY), TMA_SMEM, st>>>(m, dst, a, c, zchunk, f, idle, o);
+  dim3 grid((unsigned)((a.nx + TX - 1) / TX), (unsigned)((a.ny + T::TYT - 1) / T::TYT),
+            (unsigned)((nz_units + zchunk - 1) / zchunk));
+  built_tma_kernel<COUPLED><<<grid, dim3(TX, TY), T::SMEM, st>>>(m, dst, a, c, zchunk, f, idle, o);
   return true;
 }
 
@@ -664,7 +711,7 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
     dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TYT - 1) / TYT),
               (unsigned)((nzu + zchunk - 1) / zchunk));
     if (!use_tma() || !launch_built<false>(src_d, dst_d, *a, c, ti64_fields{}, nullptr,
-                                           CoupledODE{}, grid, zchunk, st))
+                                           CoupledODE{}, nzu, zchunk, st))
       built_pipe_kernel<false><<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk,
                                                             ti64_fields{}, nullptr, CoupledODE{});
   } else {
@@ -729,7 +776,8 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   const int zchunk = ZCHUNK;
   dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TYT - 1) / TYT),
             (unsigned)((a->z_top + zchunk - 1) / zchunk));
-  if (!use_tma() || !launch_built<true>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, grid, zchunk, st))
+  if (!use_tma() || !launch_built<true>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, a->z_top, zchunk,
+                                        st))
     built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
                                                           idle_bits_d, o);
   cudaError_t e = cudaGetLastError();
