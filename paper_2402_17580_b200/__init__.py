@@ -8,7 +8,18 @@ sm_100 device and raises ``Ti64Unavailable`` otherwise (no CPU fallback).
 
 __version__ = "0.1.0"
 
-from .kinetics import DEFAULT_PARAMS, KineticsParams, PhaseState, X_ALPHA_MAX
+from .kinetics import (
+    DEFAULT_PARAMS,
+    KineticsParams,
+    PhaseRates,
+    PhaseState,
+    X_ALPHA_MAX,
+    apply_corrections,
+    compute_rates,
+    liquid_fraction,
+    x_alpha_eq,
+    x_alpha_m_eq,
+)
 from .errors import FixedPointDivergence
 from .integrator import (
     IntegratorConfig,
@@ -25,6 +36,8 @@ from .batch import (
     AdvanceResult,
     BatchConvergenceError,
     EventCounters,
+    blend,
+    branch_dispatch,
     GlobalFields,
     advance,
     fast_exp,
@@ -38,8 +51,12 @@ from .batch import (
 from .sources import PulseHistory, PulseSweep, PulseTrain, RosenthalRaster, source_for_config
 from ._lib import Ti64Error, Ti64Unavailable
 
+from .fastmath import estrin_eval
+
 __all__ = [
-    "fast_exp", "fast_ln", "fast_pow",
+    "fast_exp", "fast_ln", "fast_pow", "estrin_eval",
+    "liquid_fraction", "x_alpha_eq", "x_alpha_m_eq", "compute_rates", "apply_corrections",
+    "PhaseRates", "blend", "branch_dispatch",
     "KineticsParams", "PhaseState", "DEFAULT_PARAMS", "X_ALPHA_MAX",
     "IntegratorConfig", "SeedingState",
     "step_explicit", "step_crank_nicolson", "integrate_interval", "integrate_history",

@@ -46,6 +46,7 @@ _SIGS = {
     "ti64_histogram": (_I64, [_P, _P, _P, _I64, _I32, _P, _P]),
     "ti64_stencil_step": (_I64, [_P, _P, _P, _P, _P, _P, _P]),
     "ti64_bench_dfma": (_I64, [_P, _I64, _I32, _P]),
+    "ti64_bench_daxpy": (_I64, [_P, _P, _D, _I64, _P]),
     "ti64_coupled_step": (_I64, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _P]),
     "ti64_last_error": (C.c_char_p, []),
     "ti64_abi_version": (_I32, []),

@@ -31,7 +31,8 @@ from .kinetics import DEFAULT_PARAMS
 __all__ = ["SUPPORTED_LANES", "BYTES_PER_POINT", "DOF_PER_POINT", "GlobalFields",
            "BatchConvergenceError", "step_all", "run_range", "advance",
            "AdvanceResult", "EventCounters", "phase_sums", "histogram",
-           "fast_exp", "fast_ln", "fast_pow", "init_from_source"]
+           "fast_exp", "fast_ln", "fast_pow", "init_from_source", "blend",
+           "branch_dispatch"]
 
 SUPPORTED_LANES = (1, 2, 4, 8)
 BYTES_PER_POINT = 72  # 5 loads + 4 stores of 8 B (batch.py:46)
@@ -138,6 +139,22 @@ class GlobalFields:
 
     def cstruct(self):
         return _abi.Fields(*[getattr(self, k).data_ptr() for k in NAMES])
+
+
+def blend(mask, a, b):
+    """Lane-wise select (batch.py:196-198)."""
+    return np.where(mask, a, b)
+
+
+def branch_dispatch(mask):
+    """'all' / 'none' / 'some' scenario of a condition mask (batch.py:201-208);
+    on the device the same decision is a warp vote over the lane group."""
+    mask = np.asarray(mask, dtype=bool)
+    if mask.all():
+        return "all"
+    if not mask.any():
+        return "none"
+    return "some"
 
 
 def _kp(params):
@@ -403,7 +420,7 @@ def _elementwise(fname, *arrays):
     b = np.broadcast_arrays(*[np.asarray(a, dtype=np.float64) for a in np_arrs])
     shape = b[0].shape
     dev = _default_device()
-    ts = [torch.from_numpy(np.ascontiguousarray(x).ravel()).to(dev) for x in b]
+    ts = [torch.from_numpy(np.array(x, dtype=np.float64).ravel()).to(dev) for x in b]
     out = torch.empty_like(ts[0])
     fn = getattr(lib, fname)
     _lib.check(fn(*[_lib.ptr(t) for t in ts], _lib.ptr(out), ts[0].numel(),

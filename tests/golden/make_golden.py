@@ -21,6 +21,9 @@ reference's own entry points:
   history.npz    integrate_history (integrator.py:303-325)
   stencil.npz    thermal._stencil_step via step_thermal (thermal.py:321-354)
   cn_steps.npz, cn_history.npz  Crank-Nicolson step_all / integrate_history
+  kinetics_api.npz  kinetics.py model functions + fastmath estrin/horner
+  report.npz     bench.count_flops / RooflineReport text, output.py VTK
+                 snapshots and probe CSV of a micro build
   build.npz      thermal.run_build on the reference's micro build
                  (test_thermal.py:33-43, :192-200): final thermal field, all
                  kinetics arrays, probe rows, for several scan strategies /
@@ -429,7 +432,110 @@ def make_build():
     np.savez_compressed(OUT / "build.npz", **cases)
 
 
+def make_report():
+    """bench.count_flops / RooflineReport (bench.py:158-257) and the output
+    writers (output.py) on reference states."""
+    import tempfile
+    from ti64micro import bench as rb, output as ro
+    from ti64micro.scanpath import ScanPath, serpentine
+    cases = {}
+    for block in (1, 10, 100):
+        lay = generate_layout(block, 1000 + block, seed=block)
+        for k in NAMES[:5]:
+            cases[f"layout{block}/{k}"] = np.array(getattr(lay, k))
+        for lanes in (1, 8):
+            cases[f"layout{block}/flops_explicit_l{lanes}"] = np.int64(
+                rb.count_flops(lay, "explicit", lanes))
+        it = np.arange(lay.n_points) % 5
+        cases[f"layout{block}/iters"] = it
+        cases[f"layout{block}/flops_cn_l8"] = np.int64(
+            rb.count_flops(lay, "crank_nicolson", 8, iters=it))
+    runs = [dict(label="explicit_b1", flops=123456789, bytes=72 * 400000, seconds=0.0123),
+            dict(label="cn_b100", flops=987654321, bytes=72 * 400000, seconds=0.0456)]
+    rep = rb.roofline(runs, measured_bandwidth=6538.0, peak_flops=34120.5,
+                      instruction_mix_factor=0.57)
+    cases["roofline/csv"] = np.array(rep.to_csv())
+    cases["roofline/gnuplot"] = np.array(rep.to_gnuplot())
+    cases["roofline/respects"] = np.array(rep.respects_ceilings())
+    cases["roofline/mem_dof"] = np.float64(rep.memory_bound_dof_rate)
+    MM = 1e-3
+    geom = th.BuildGeometry(plate_size=(0.6 * MM, 0.6 * MM, 0.15 * MM),
+                            part_size=(0.4 * MM, 0.4 * MM, 0.1 * MM), voxel=0.05 * MM)
+    sched = th.BuildSchedule(dt_active=2e-5, interlayer_dwell=0.02, initial_dwell_steps=50,
+                             final_cooldown=0.05, preheat=293.0)
+    segs = []
+    for layer in range(geom.grid[3]):
+        segs.extend(serpentine(geom.part_extent, 0.08 * MM, 0.96, 180.0, layer))
+    scan = ScanPath(segs, dwell=sched.interlayer_dwell)
+    snaps = {}
+
+    def hook(label, t, field, fields):
+        with tempfile.NamedTemporaryFile("r", suffix=".vtk") as tf:
+            ro.write_vtk_snapshot(tf.name, field, fields, label=label)
+            snaps[label] = open(tf.name).read()
+
+    field, fields, probes = th.run_build(geom, scan, sched, snapshot_hook=hook,
+                                         probe_points=[(0.3 * MM, 0.3 * MM, 0.17 * MM)])
+    for label, text in snaps.items():
+        cases[f"vtk/{label}"] = np.array(text)
+    with tempfile.NamedTemporaryFile("r", suffix=".csv") as tf:
+        ro.write_probe_csv(tf.name, probes[0])
+        cases["csv/probe0"] = np.array(open(tf.name).read())
+    cases["sched"] = np.array([sched.dt_active, sched.interlayer_dwell,
+                               sched.initial_dwell_steps, sched.growth_every, sched.dt_max,
+                               sched.final_cooldown, sched.preheat, sched.room])
+    np.savez_compressed(OUT / "report.npz", **cases)
+
+
+def make_kinetics_api():
+    """kinetics.py:144-269 model functions and fastmath estrin/horner helpers
+    on seeded inputs (scalars and arrays)."""
+    from ti64micro import kinetics as rk
+    from ti64micro.fastmath import estrin_eval, horner_eval, EXP_CORRECTION, LN_CORRECTION
+    rng = np.random.default_rng(5)
+    t = np.concatenate([rng.uniform(250.0, 2100.0, 400),
+                        [848.0, 935.0, 1273.0, 1373.0, 1878.0, 1928.0, 850.0, 300.0]])
+    xs = rng.uniform(-0.05, 0.95, t.size)
+    xm = rng.uniform(-0.05, 0.9, t.size)
+    xs[:20] = 0.0
+    xm[20:40] = 0.0
+    c = {"t": t, "xs": xs, "xm": xm}
+    c["liquid_fraction"] = rk.liquid_fraction(t)
+    c["solid_fraction"] = rk.solid_fraction(t)
+    c["x_alpha_eq"] = rk.x_alpha_eq(t)
+    c["x_alpha_m_eq"] = rk.x_alpha_m_eq(t, xs)
+    c["k_as"], c["k_b"] = rk.diffusion_rate_k(t)
+    r = rk.compute_rates((xs, xm), t)
+    c["ds"], c["dm"] = r.d_x_alpha_s, r.d_x_alpha_m
+    st = rk.apply_corrections((xs, xm), t)
+    c["cxs"], c["cxm"], c["cxb"] = st.x_alpha_s, st.x_alpha_m, st.x_beta
+    sc = [(0.3, 0.2, 950.0), (0.0, 0.0, 1000.0), (0.9, 0.0, 1200.0), (0.5, 0.4, 700.0)]
+    c["scalar_in"] = np.array(sc)
+    out = []
+    for a, b, tt in sc:
+        rr = rk.compute_rates(rk.PhaseState(a, b, 0.0), tt)
+        cc = rk.apply_corrections(rk.PhaseState(a, b, 0.0), tt)
+        out.append([rr.d_x_alpha_s, rr.d_x_alpha_m, cc.x_alpha_s, cc.x_alpha_m, cc.x_beta,
+                    rk.x_alpha_eq(tt), rk.liquid_fraction(tt)])
+    c["scalar_out"] = np.array(out)
+    y = rng.uniform(0.0, 1.0, 100)
+    c["y"] = y
+    c["estrin_exp"] = estrin_eval(EXP_CORRECTION, y)
+    c["estrin_ln"] = estrin_eval(LN_CORRECTION, y)
+    c["estrin_odd"] = estrin_eval((1.0, -0.5, 0.25, 0.125, -1.5), y)
+    c["horner_ln"] = horner_eval(LN_CORRECTION, y)
+    np.savez_compressed(OUT / "kinetics_api.npz", **c)
+
+
 if __name__ == "__main__":
+    if "--api-only" in sys.argv:
+        make_kinetics_api()
+        print("kinetics api done")
+        sys.exit(0)
+    if "--report-only" in sys.argv:
+        make_report()
+        print("report done")
+        sys.exit(0)
     if "--build-only" in sys.argv:
         make_build()
         print("build done")
@@ -442,6 +548,10 @@ if __name__ == "__main__":
     print("cn done")
     make_build()
     print("build done")
+    make_report()
+    print("report done")
+    make_kinetics_api()
+    print("kinetics api done")
     make_fastmath()
     print("fastmath done")
     make_steps()
