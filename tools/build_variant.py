@@ -1,25 +1,48 @@
-"""Build a variant of libti64b200.so with extra -D flags (A/B experiments):
-    python tools/build_variant.py NAME -DFOO=1 ...   -> _lib/variants/lib_NAME.so
-Select it at run time with TI64_LIB=<path>."""
+"""Build a variant of libti64b200.so for A/B experiments:
+    python tools/build_variant.py NAME [--rev GITREV] [-DFOO=1 ...]
+        -> paper_2402_17580_b200/_lib/variants/lib_NAME.so
+--rev builds the sources (csrc + include) of that git revision instead of the
+working tree.  Select a variant at run time with TI64_LIB=<path>."""
 import subprocess
 import sys
+import tempfile
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2402_17580_b200 import _build as b  # noqa: E402
 
-name, defs = sys.argv[1], sys.argv[2:]
+args = sys.argv[1:]
+name = args.pop(0)
+rev = None
+if "--rev" in args:
+    i = args.index("--rev")
+    rev = args[i + 1]
+    del args[i:i + 2]
+defs = args
 out = b.OUT_DIR / "variants"
 out.mkdir(parents=True, exist_ok=True)
-objs = []
-for s in b.SOURCES:
-    o = out / f"{Path(s).stem}_{name}.o"
-    subprocess.run([b.nvcc(), *b.NVCC_FLAGS, *defs, "-I", str(b.ROOT / "include"), "-c",
-                    str(b.CSRC / s), "-o", str(o)], check=True)
-    objs.append(str(o))
-lib = out / f"lib_{name}.so"
-subprocess.run([b.nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o",
-                str(lib), *objs, "-cudart", "static"], check=True)
-for o in objs:
-    Path(o).unlink()
+with tempfile.TemporaryDirectory() as tmp:
+    if rev:
+        root = Path(tmp)
+        (root / "pkg" / "csrc").mkdir(parents=True)
+        (root / "include").mkdir()
+        for f in b.SOURCES + b.HEADERS:
+            txt = subprocess.run(["git", "show", f"{rev}:paper_2402_17580_b200/csrc/{f}"],
+                                 capture_output=True, text=True, cwd=b.ROOT).stdout
+            (root / "pkg" / "csrc" / f).write_text(txt)
+        (root / "include" / "ti64_b200.h").write_text(subprocess.run(
+            ["git", "show", f"{rev}:include/ti64_b200.h"], capture_output=True, text=True,
+            cwd=b.ROOT).stdout)
+        csrc, inc = root / "pkg" / "csrc", root / "include"
+    else:
+        csrc, inc = b.CSRC, b.ROOT / "include"
+    objs = []
+    for s in b.SOURCES:
+        o = Path(tmp) / f"{Path(s).stem}.o"
+        subprocess.run([b.nvcc(), *b.NVCC_FLAGS, *defs, "-I", str(inc), "-c", str(csrc / s),
+                        "-o", str(o)], check=True)
+        objs.append(str(o))
+    lib = out / f"lib_{name}.so"
+    subprocess.run([b.nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o",
+                    str(lib), *objs, "-cudart", "static"], check=True)
 print(lib)
