@@ -113,16 +113,33 @@ class RosenthalRaster:
             out[n, 2] = d
         return out
 
+    def straight_runs(self, tab):
+        """Per row r: how many rows from r on (r included) continue one
+        straight pass — same y, same direction, x advancing by exactly
+        dir * speed * dt (to 1e-12 m).  The kernel's multi-step rest bound is
+        only applied inside such a run."""
+        n = len(tab)
+        step = self.speed * self.dt
+        run = np.ones(n, np.int64)
+        if n > 1:
+            ok = ((tab[1:, 1] == tab[:-1, 1]) & (tab[1:, 2] == tab[:-1, 2]) &
+                  (np.abs(tab[1:, 0] - tab[:-1, 0] - tab[:-1, 2] * step) <= 1e-12))
+            for r in range(n - 2, -1, -1):
+                if ok[r]:
+                    run[r] = run[r + 1] + 1
+        return np.minimum(run, 1 << 24)
+
     def packed_beam(self, n_rows):
         """Device layout of the beam table: the (n_rows, 3) doubles, padded to
-        an even count, then n_rows float32 rows (x, y, dir, 0) for the kernel's
-        FP32 no-op filter; returned as one float64 array."""
+        an even count, then n_rows float32 rows (x, y, dir, run) for the
+        kernel's FP32 filters (run = straight_runs); one float64 array."""
         tab = self.beam_table(n_rows)
         nd = 3 * n_rows + (3 * n_rows) % 2
         out = np.zeros(nd + 2 * n_rows)
         out[:3 * n_rows] = tab.ravel()
         f = np.zeros((n_rows, 4), np.float32)
         f[:, :3] = tab
+        f[:, 3] = self.straight_runs(tab)
         out[nd:] = f.view(np.float64).ravel()
         return out
 
@@ -164,6 +181,7 @@ class RosenthalRaster:
         g.pf[1] = coef
         g.pf[2] = vk * 1.4426950408889634
         g.pf[3] = thr / vk
+        g.pf[4] = self.speed * self.dt  # beam advance per row inside a straight run
         return g
 
 
