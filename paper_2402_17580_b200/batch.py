@@ -312,12 +312,12 @@ def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
                           int(n_lanes), int(snapshot_every), C.byref(kp), C.byref(cfg),
                           None if cs is None else C.byref(cs), _lib.ptr(sums),
                           _lib.ptr(scratch), _lib.stream_handle(stream))
-    _lib.check(rc, "ti64_advance")
+    launches = _lib.check(rc, "ti64_advance")  # >= 0: kernels launched
     del beam  # kernels are queued; the cache keeps the table alive
     fields.traffic_bytes += BYTES_PER_POINT * n * n_steps
     fields.steps_taken += n_steps
     return AdvanceResult(sums=sums[:n_snap], counters=counters, steps=n_steps,
-                         launches=3 * n_snap)
+                         launches=int(launches))
 
 
 def init_from_source(source, n, point_offset=0, device=None):
