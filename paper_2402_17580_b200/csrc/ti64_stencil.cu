@@ -19,6 +19,7 @@
 #include <cuda.h>  // CUtensorMap (types only; the encoder comes via cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -637,11 +638,15 @@ bool launch_built(const double* src, double* dst, const ti64_stencil_args& a,
   using T = TileOf<COUPLED>;
   CUtensorMap m;
   if (!make_plane_map(&m, src, a.nx, a.ny, a.nz_stored, T::BOX_Y)) return false;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the opt-in shared-memory size is a per-device function attribute
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
     cudaFuncSetAttribute(built_tma_kernel<COUPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          T::SMEM);
-    attr_set = true;
+    attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   dim3 grid((unsigned)((a.nx + TX - 1) / TX), (unsigned)((a.ny + T::TYT - 1) / T::TYT),
             (unsigned)((nz_units + zchunk - 1) / zchunk));
