@@ -21,6 +21,8 @@ reference's own entry points:
   history.npz    integrate_history (integrator.py:303-325)
   stencil.npz    thermal._stencil_step via step_thermal (thermal.py:321-354)
   cn_steps.npz, cn_history.npz  Crank-Nicolson step_all / integrate_history
+  acceptance.npz the reference's acceptance-criterion quantities
+                 (test_acceptance.py), incl. the coupled cube builds
   kinetics_api.npz  kinetics.py model functions + fastmath estrin/horner
   report.npz     bench.count_flops / RooflineReport text, output.py VTK
                  snapshots and probe CSV of a micro build
@@ -527,7 +529,106 @@ def make_kinetics_api():
     np.savez_compressed(OUT / "kinetics_api.npz", **c)
 
 
+def make_acceptance():
+    """The reference's acceptance-criterion quantities (test_acceptance.py:51-361)
+    computed by the reference itself; the GPU suite reproduces them."""
+    import math
+    from ti64micro import fastmath as rfm
+    from ti64micro.integrator import analytic_beta_growth
+    from ti64micro.kinetics import PhaseState, liquid_fraction
+    from ti64micro.scanpath import ScanPath, serpentine, four_islands
+    CFG_I = IntegratorConfig(scheme="crank_nicolson")
+    c = {}
+    # 2: lane equivalence of the implicit scheme (max deviation vs 1 lane)
+    base = random_states(10_000, seed=21)
+    ref = base.copy()
+    step_all(ref, 0.01, DEFAULT_PARAMS, CFG_I, n_lanes=1)
+    c["c2_ref_states"] = ref.states()
+    for lanes in (2, 4, 8):
+        f = base.copy()
+        step_all(f, 0.01, DEFAULT_PARAMS, CFG_I, n_lanes=lanes)
+        c[f"c2_states_l{lanes}"] = f.states()
+    c["c2_in"] = np.stack([base.x_alpha_s, base.x_alpha_m, base.x_beta,
+                           base.temperature_old, base.temperature_new])
+    # 3: continuity over 100 seeded histories, both schemes
+    rng = np.random.default_rng(33)
+    worst = 0.0
+    for _ in range(100):
+        knots_t = np.concatenate([[0.0], np.sort(rng.uniform(0.1, 6.0, 5))])
+        knots_T = rng.uniform(293.0, 2000.0, 6)
+        times = np.linspace(0.0, knots_t[-1], 1500)
+        temps = np.interp(times, knots_t, knots_T)
+        for cfg in (CFG_E, CFG_I):
+            out = integrate_history(times, temps, config=cfg)
+            worst = max(worst, float(np.abs(out.sum(axis=1) - (1.0 - liquid_fraction(temps))).max()))
+    c["c3_worst"] = np.float64(worst)
+    # 4: equilibrium convergence under CN holds
+    finals = []
+    for t_hold in (1000.0, 1100.0, 1200.0):
+        times = np.arange(0.0, 10_000.0 + 0.5, 1.0)
+        temps = np.full_like(times, t_hold)
+        out = integrate_history(times, temps, state0=PhaseState(0.0, 0.0, 1.0), config=CFG_I)
+        finals.append(out[-1])
+    c["c4_finals"] = np.array(finals)
+    # 5: Appendix-A closed form
+    for scheme, dt in (("explicit", 1e-4), ("crank_nicolson", 1e-2)):
+        n = int(round(1000.0 / dt))
+        times = dt * np.arange(n + 1)
+        temps = np.full(n + 1, 1200.0)
+        out = integrate_history(times, temps, state0=PhaseState(0.9, 0.0, 0.1),
+                                config=IntegratorConfig(scheme=scheme))
+        _, exact = analytic_beta_growth(1200.0, dt, n)
+        c[f"c5_{scheme}_err"] = np.float64(np.abs(out[1:, 2] - exact).max())
+        c[f"c5_{scheme}_xb_tail"] = out[-1000:, 2]
+    # 6: explicit (1e-5) vs CN (1e-3) along a 10 s cooling ramp
+    t_end = 10.0
+    times_e = np.arange(0.0, t_end + 1e-9, 1e-5)
+    temps_e = 1300.0 + (300.0 - 1300.0) * times_e / t_end
+    out_e = integrate_history(times_e, temps_e, config=CFG_E)
+    times_i = np.arange(0.0, t_end + 1e-9, 1e-3)
+    temps_i = 1300.0 + (300.0 - 1300.0) * times_i / t_end
+    out_i = integrate_history(times_i, temps_i, config=CFG_I)
+    checks = np.linspace(0.1, 10.0, 100)
+    c["c6_e"] = out_e[np.searchsorted(times_e, checks)]
+    c["c6_i"] = out_i[np.searchsorted(times_i, checks)]
+    # 7 / 8: the coupled cube builds
+    MM = 1e-3
+
+    def cube(geometry, strategy, schedule):
+        segs = []
+        for layer in range(geometry.grid[3]):
+            segs.extend(strategy(geometry.part_extent, 0.08 * MM, 0.96, 180.0, layer))
+        scan = ScanPath(segs, dwell=schedule.interlayer_dwell)
+        source = th.HeatSource(w_eff=180.0, radius=0.06 * MM, h_powder=geometry.voxel)
+        return th.run_build(geometry, scan, schedule, source=source)
+
+    g7 = th.BuildGeometry(plate_size=(1.2 * MM, 1.2 * MM, 0.2 * MM),
+                          part_size=(1.0 * MM, 1.0 * MM, 0.25 * MM), voxel=0.05 * MM)
+    s7 = th.BuildSchedule(dt_active=2e-5, interlayer_dwell=1.0, initial_dwell_steps=2000,
+                          final_cooldown=20.0, preheat=293.0)
+    f7, k7, _ = cube(g7, serpentine, s7)
+    for k in NAMES:
+        c[f"c7_{k}"] = np.array(getattr(k7, k))
+    c["c7_r_c"], c["c7_state"] = np.array(f7.r_c), np.array(f7.state)
+    g8 = th.BuildGeometry(plate_size=(1.0 * MM, 1.0 * MM, 3.0 * MM),
+                          part_size=(1.0 * MM, 1.0 * MM, 1.0 * MM), voxel=0.05 * MM)
+    s8 = th.BuildSchedule(dt_active=2e-5, interlayer_dwell=0.35, initial_dwell_steps=500,
+                          final_cooldown=10.0, preheat=600.0)
+    for name, strat in (("single", serpentine), ("islands", four_islands)):
+        f8, k8, _ = cube(g8, strat, s8)
+        c[f"c8_{name}_xs"] = np.array(k8.x_alpha_s)
+        c[f"c8_{name}_xm"] = np.array(k8.x_alpha_m)
+        c[f"c8_{name}_r_c"] = np.array(f8.r_c)
+        c[f"c8_{name}_state"] = np.array(f8.state)
+        c[f"c8_{name}_T"] = np.array(f8.temperature_old)
+    np.savez_compressed(OUT / "acceptance.npz", **c)
+
+
 if __name__ == "__main__":
+    if "--acceptance-only" in sys.argv:
+        make_acceptance()
+        print("acceptance done")
+        sys.exit(0)
     if "--api-only" in sys.argv:
         make_kinetics_api()
         print("kinetics api done")
@@ -552,6 +653,8 @@ if __name__ == "__main__":
     print("report done")
     make_kinetics_api()
     print("kinetics api done")
+    make_acceptance()
+    print("acceptance done")
     make_fastmath()
     print("fastmath done")
     make_steps()
