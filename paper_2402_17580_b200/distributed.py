@@ -93,7 +93,8 @@ class SlabCoupledDriver:
     temperature buffers; `send/recv` move one plane.
     """
 
-    def __init__(self, nz, ny, nx, rank, world, t_old, t_new, stencil, step, exchange):
+    def __init__(self, nz, ny, nx, rank, world, t_old, t_new, stencil, step, exchange,
+                 overlap=True):
         self.nz, self.ny, self.nx = nz, ny, nx
         self.rank, self.world = rank, world
         self.z0, self.z1 = slab_range(nz, rank, world)
@@ -101,6 +102,8 @@ class SlabCoupledDriver:
         self.ze = min(self.z1 + 1, nz)
         self.t_old, self.t_new = t_old, t_new  # (ze - zb, ny, nx)
         self.stencil, self.step_fn, self.exchange = stencil, step, exchange
+        self.overlap = overlap
+        self._halos_current = False
 
     @property
     def slab(self):
@@ -122,25 +125,74 @@ class SlabCoupledDriver:
             ops.append(("recv", self.t_old[hi], self.rank + 1))
         self.exchange(ops)
 
+    def _edge_ops(self):
+        """T_{n+1} of my edge planes straight into the neighbours' T_old halo
+        planes (their next step's T_n), their edges into mine."""
+        lo, hi = self.z0 - self.zb, self.z1 - self.zb
+        ops = []
+        if self.rank > 0:
+            ops.append(("send", self.t_new[lo], self.rank - 1))
+            ops.append(("recv", self.t_old[lo - 1], self.rank - 1))
+        if self.rank < self.world - 1:
+            ops.append(("send", self.t_new[hi - 1], self.rank + 1))
+            ops.append(("recv", self.t_old[hi], self.rank + 1))
+        return ops
+
     def run_step(self, dt, args_for):
-        """One coupled step: halos, K4 on own planes, kinetics on own cells."""
-        self.halo_exchange()
-        self.stencil(self.t_old, self.t_new, args_for(self.slab))
+        """One coupled step: K4 on own planes, kinetics on own cells.
+
+        overlap=False: blocking halo swap of T_n, then the whole slab.
+        overlap=True (default): the two edge planes first, then their new
+        values go out to the neighbours' halos asynchronously while the
+        interior planes and the kinetics run; the transfer only has to land
+        before the next step's edge planes.  Ordering makes it race-free: a
+        halo is overwritten only after this rank's edge planes consumed it,
+        the sends read T_{n+1} (the kinetics roll touches T_old of owned
+        cells only), and the interior planes never read a halo.
+        """
         lo, hi = self.owned_flat_range()
+        if not self.overlap:
+            self.halo_exchange()
+            self.stencil(self.t_old, self.t_new, args_for(self.slab))
+            self.step_fn(lo, hi, dt)
+            return
+        if not self._halos_current:
+            self.halo_exchange()  # first step: halos of the initial T_old
+            self._halos_current = True
+        zb, nzs = self.zb, self.ze - self.zb
+        for z in sorted({self.z0, self.z1 - 1}):
+            self.stencil(self.t_old, self.t_new, args_for((zb, nzs, z, z + 1)))
+        pending = self.exchange(self._edge_ops(), wait=False)
+        if self.z1 - self.z0 > 2:
+            self.stencil(self.t_old, self.t_new, args_for((zb, nzs, self.z0 + 1, self.z1 - 1)))
         self.step_fn(lo, hi, dt)
+        pending.wait()
 
 
-def torch_exchange(ops):
-    """Point-to-point plane exchange with torch.distributed (NCCL or gloo)."""
+class _Pending:
+    def __init__(self, reqs):
+        self.reqs = reqs
+
+    def wait(self):
+        # NCCL: the current stream waits for the transfer (the host does not);
+        # gloo: the host waits
+        for r in self.reqs:
+            r.wait()
+        self.reqs = []
+
+
+def torch_exchange(ops, wait=True):
+    """Point-to-point plane exchange with torch.distributed (NCCL or gloo).
+    wait=False returns a handle whose wait() completes the exchange; NCCL
+    orders the sends after the work already queued on the current stream,
+    so later kernels overlap the transfer."""
     import torch.distributed as dist
-    reqs = []
-    p2p = []
-    for kind, tensor, peer in ops:
-        p2p.append(dist.P2POp(dist.isend if kind == "send" else dist.irecv, tensor, peer))
-    if p2p:
-        reqs = dist.batch_isend_irecv(p2p)
-    for r in reqs:
-        r.wait()
+    p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, tensor, peer)
+           for kind, tensor, peer in ops]
+    pending = _Pending(dist.batch_isend_irecv(p2p) if p2p else [])
+    if wait:
+        pending.wait()
+    return pending
 
 
 def gather_planes(local, z0, z1, zb, nz, world, rank):

@@ -118,7 +118,7 @@ def _coupled_reference():
     return f
 
 
-def _slab_worker(rank, world, port, q):
+def _slab_worker(rank, world, port, q, overlap=True):
     from oracle import oracle as orc
     from paper_2402_17580_b200 import _abi
     from paper_2402_17580_b200.thermal import DEFAULT_THERMAL, HeatSource
@@ -152,7 +152,7 @@ def _slab_worker(rank, world, port, q):
         to[:] = hf.temperature_old
 
     drv = D.SlabCoupledDriver(NZ, NY, NX, rank, world, t_old, t_new, stencil, step,
-                              D.torch_exchange)
+                              D.torch_exchange, overlap=overlap)
 
     def args_for(slab):
         k = beam_k[0]
@@ -172,11 +172,14 @@ def _slab_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_zslab_halo_exchange_equals_whole_grid(world):
+@pytest.mark.parametrize("world,overlap", [(2, False), (2, True), (3, True), (7, True)])
+def test_zslab_halo_exchange_equals_whole_grid(world, overlap):
+    """Blocking swap and the overlapped schedule (edge planes, async halo
+    send of T_{n+1}, interior + kinetics) both equal the whole-grid run
+    bitwise; world 7 puts 1- and 2-plane slabs (no interior) in play."""
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
-    mp.start_processes(_slab_worker, args=(world, _free_port(), q), nprocs=world,
+    mp.start_processes(_slab_worker, args=(world, _free_port(), q, overlap), nprocs=world,
                        start_method="spawn")
     t_all, parts = q.get()
     ref = _coupled_reference()
