@@ -61,7 +61,12 @@ def _to_device(a, dtype, n, name, device):
         t = a.detach()
     else:
         t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.dtype(dtype))))
-    t = t.to(device=device, dtype=getattr(torch, dtype)).contiguous()
+    if device.type == "cpu":  # host-resident fields: pinned, mapped into the GPU (UVA)
+        t = t.to(device="cpu", dtype=getattr(torch, dtype)).contiguous()
+        if not t.is_pinned():
+            t = t.pin_memory()
+    else:
+        t = t.to(device=device, dtype=getattr(torch, dtype)).contiguous()
     if tuple(t.shape) != (n,):
         raise ValueError(f"field {name} must have shape ({n},)")
     return t
@@ -70,7 +75,15 @@ def _to_device(a, dtype, n, name, device):
 @dataclass
 class GlobalFields:
     """The five global state vectors plus per-point seeding bookkeeping,
-    resident on the GPU (batch.py:99-146)."""
+    resident on the GPU (batch.py:99-146).
+
+    device="host" keeps them in pinned host memory instead, mapped into the
+    GPU's address space: the kernels then read their inputs from and write
+    their results to host memory themselves (zero-copy).  For the fused
+    advance, which touches each point's state once at the start and once at
+    the end of the launch, the host-link transfer overlaps the computation
+    of other points — the end-to-end path for data that lives on the host.
+    Host reads (states/host/to_host) synchronise the device first."""
 
     x_alpha_s: object
     x_alpha_m: object
@@ -89,6 +102,11 @@ class GlobalFields:
         for name in _F64[:5]:
             if tuple(np.shape(getattr(self, name))) != (n,) or n < 0:
                 raise ValueError(f"field {name} must have shape ({max(n, 0)},)")
+        torch = _torch()
+        if self.device == "host" or (isinstance(self.device, torch.device) and
+                                     self.device.type == "cpu"):
+            _lib.require()
+            self.device = torch.device("cpu")
         dev = self.device if self.device is not None else _default_device()
         self.device = dev
         for name in _F64[:5]:
@@ -96,18 +114,29 @@ class GlobalFields:
         torch = _torch()
         if self.seed_tracked is None:
             self.seed_tracked = torch.zeros(n, dtype=torch.float64, device=dev)
-        else:
-            self.seed_tracked = _to_device(self.seed_tracked, "float64", n, "seed_tracked", dev)
+        self.seed_tracked = _to_device(self.seed_tracked, "float64", n, "seed_tracked", dev)
         for name in _U8:
             v = getattr(self, name)
             if v is None:
-                setattr(self, name, torch.zeros(n, dtype=torch.uint8, device=dev))
-            else:
-                setattr(self, name, _to_device(v, "uint8", n, name, dev))
+                v = torch.zeros(n, dtype=torch.uint8, device=dev)
+            setattr(self, name, _to_device(v, "uint8", n, name, dev))  # (pins host arrays)
 
     @property
     def n_points(self):
         return int(self.x_alpha_s.shape[0])
+
+    @property
+    def host_resident(self):
+        return self.device.type == "cpu"
+
+    @property
+    def compute_device(self):
+        """The CUDA device the kernels run on (scratch, sums, iteration counts)."""
+        return _default_device() if self.host_resident else self.device
+
+    def _sync_host(self):
+        if self.host_resident:
+            _torch().cuda.synchronize()
 
     @classmethod
     def allocate(cls, n, temperature=293.0, device=None):
@@ -120,6 +149,7 @@ class GlobalFields:
         `out`: optional (n, 3) float64 host tensor (pin it for full D2H
         bandwidth) that receives the copy; its numpy view is returned."""
         torch = _torch()
+        self._sync_host()
         st = torch.stack([self.x_alpha_s, self.x_alpha_m, self.x_beta], 1)
         if out is None:
             return st.cpu().numpy()
@@ -127,6 +157,7 @@ class GlobalFields:
         return out.numpy()
 
     def host(self, name):
+        self._sync_host()
         return getattr(self, name).cpu().numpy()
 
     def to_host(self):
@@ -202,7 +233,7 @@ def step_all(fields, dt, params=DEFAULT_PARAMS, config=IntegratorConfig(), n_lan
     nsub = num_substeps(float(dt), config.dt_sub_max)
     iters = None
     if record_iters:
-        iters = _torch().zeros(n, dtype=_torch().int64, device=fields.device)
+        iters = _torch().zeros(n, dtype=_torch().int64, device=fields.compute_device)
     rc = run_range(fields, 0, n, n_lanes, nsub, float(dt) / nsub, params.kernel_tuple(),
                    config.kernel_tuple(), record_iters, iters, stream)
     fields.traffic_bytes += BYTES_PER_POINT * n
@@ -298,7 +329,7 @@ def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
     lib = _lib.require()
     torch = _torch()
     n = fields.n_points
-    dev = fields.device
+    dev = fields.compute_device
     nsub = num_substeps(float(source.dt), config.dt_sub_max)
     g, beam = tempgen_for(source, point_offset, step0 + n_steps + 1, dev)
     chunk = snapshot_every if snapshot_every > 0 else max(n_steps, 1)
@@ -349,7 +380,7 @@ def _advance_implicit(fields, n_steps, source, step0, params, config, n_lanes,
     lib = _lib.require()
     torch = _torch()
     n = fields.n_points
-    dev = fields.device
+    dev = fields.compute_device
     g, beam = tempgen_for(source, point_offset, step0 + n_steps + 1, dev)
     chunk = snapshot_every if snapshot_every > 0 else max(n_steps, 1)
     n_snap = (n_steps + chunk - 1) // chunk if n_steps > 0 else 0
@@ -388,8 +419,8 @@ def phase_sums(fields, scratch=None):
     """Deterministic fp64 sums (x_alpha_s, x_alpha_m, x_beta) -> tensor(3)."""
     lib = _lib.require()
     torch = _torch()
-    out = torch.zeros(3, dtype=torch.float64, device=fields.device)
-    scratch = _scratch(fields.n_points, fields.device) if scratch is None else scratch
+    out = torch.zeros(3, dtype=torch.float64, device=fields.compute_device)
+    scratch = _scratch(fields.n_points, fields.compute_device) if scratch is None else scratch
     _lib.check(lib.ti64_phase_sums(_lib.ptr(fields.x_alpha_s), _lib.ptr(fields.x_alpha_m),
                                    _lib.ptr(fields.x_beta), fields.n_points, _lib.ptr(out),
                                    _lib.ptr(scratch), _lib.stream_handle()), "ti64_phase_sums")
@@ -401,7 +432,7 @@ def histogram(fields, nbins=256, out=None):
     lib = _lib.require()
     torch = _torch()
     if out is None:
-        out = torch.zeros((3, nbins), dtype=torch.int64, device=fields.device)
+        out = torch.zeros((3, nbins), dtype=torch.int64, device=fields.compute_device)
     _lib.check(lib.ti64_histogram(_lib.ptr(fields.x_alpha_s), _lib.ptr(fields.x_alpha_m),
                                   _lib.ptr(fields.x_beta), fields.n_points, int(nbins),
                                   _lib.ptr(out), _lib.stream_handle()), "ti64_histogram")

@@ -286,3 +286,24 @@ def test_phase_sums_and_histogram(pkg):
         x = d[k]
         ref = np.bincount(np.clip(np.floor(x * 256).astype(np.int64), 0, 255), minlength=256)
         assert np.array_equal(hist[c], ref)
+
+
+def test_host_resident_fields_zero_copy(pkg):
+    """GlobalFields(device='host'): pinned host state read and written by the
+    kernels themselves gives the same bits as device-resident state."""
+    src = pkg.RosenthalRaster(nx=64, ny=64, nz=8)
+    n = src.n_points
+    a = pkg.init_from_source(src, n)
+    h = pkg.GlobalFields(*[a.host(k) for k in FIELD_NAMES], device="host")
+    assert h.host_resident and h.x_alpha_s.is_pinned()
+    ra = pkg.advance(a, 700, src, snapshot_every=300)
+    rh = pkg.advance(h, 700, src, snapshot_every=300)
+    assert_fields(h, a.to_host(), "advance host vs device")
+    assert np.array_equal(rh.sums.cpu().numpy(), ra.sums.cpu().numpy())
+    d = random_states(5000, seed=9)
+    b = pkg.GlobalFields(*[d[k] for k in FIELD_NAMES[:5]])
+    g = pkg.GlobalFields(*[d[k] for k in FIELD_NAMES[:5]], device="host")
+    for cfg in (pkg.IntegratorConfig(), pkg.IntegratorConfig(scheme="crank_nicolson")):
+        pkg.step_all(b, 1e-3, config=cfg)
+        pkg.step_all(g, 1e-3, config=cfg)
+        assert_fields(g, b.to_host(), f"step_all host vs device {cfg.scheme}")
