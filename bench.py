@@ -35,7 +35,10 @@ sys.path.insert(0, str(ROOT))
 METRIC = "microstructure point-updates/s (fp64)"
 UNIT = "point-updates/s"
 JOB_STEPS = 10_000
-SNAP_EVERY = int(os.environ.get("TI64_BENCH_SNAP", "1000"))  # steps per fused launch
+SNAP_EVERY = int(os.environ.get("TI64_BENCH_SNAP", "1000"))  # snapshot interval (steps)
+# DRAM bytes (read + write) of the job's single K2 launch, from the committed
+# ncu capture profiles/r01_advance_cfg1_job.txt (44.87 MB + 8.89 MB)
+K2_JOB_DRAM_BYTES = 44_866_816 + 8_892_160
 WORKLOAD = ("config1: Rosenthal raster (200 W, eta 0.35, 1 m/s, 100 um hatch), "
             "N=2^20 points on 128x128x64 lattice h=20um, 10000 steps dt=2e-5 s, "
             "state (0.9,0,0.1)")
@@ -492,7 +495,11 @@ def run_b200(args):
                        "l2": "flushed between timed iterations (256 MiB write)",
                        "parallelism": f"points sharded, {world} replica(s) of the job"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf,
-                         "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peak_tf,
+                         "traffic": K2_JOB_DRAM_BYTES,
+                         "traffic_source": "ncu --set full of this job's K2 launch "
+                                           "(profiles/r01_advance_cfg1_job.txt): "
+                                           "dram read + write bytes per launch",
                          "peak_source": "measured on this box: DFMA stream (ti64_bench_dfma)",
                          "flops_per_update": flops_job / upd_job,
                          "kernel": "advance_kernel<ROSENTHAL>"},

@@ -19,6 +19,7 @@ ap.add_argument("--step0", type=int, default=0)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--pre", type=int, default=0, help="untimed steps before the measured launches")
+ap.add_argument("--snap", type=int, default=0, help="snapshot_every of the measured launches")
 a = ap.parse_args()
 src = pkg.source_for_config(a.config)
 n = a.n or (src.n_points if a.config == 1 else {0: 4096, 2: 1 << 24, 4: 1 << 24}[a.config])
@@ -33,7 +34,7 @@ for r in range(a.reps):
     f = f0.copy()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    pkg.advance(f, a.steps, src, step0=a.step0)
+    pkg.advance(f, a.steps, src, step0=a.step0, snapshot_every=a.snap)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)

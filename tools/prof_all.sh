@@ -20,10 +20,10 @@ run cn python tools/cn_probe.py && \
   ncu --set full --import-source on --clock-control none -k regex:run_range_cn \
       --launch-skip 1 -c 1 -o gpurun_out/prof_cn -f python tools/cn_probe.py \
       > gpurun_out/ncu_cn.log 2>&1
-run adv1 python tools/prof_advance.py --pre 4000 --reps 1 && \
+run adv1 python tools/prof_advance.py --steps 10000 --snap 1000 --reps 1 && \
   ncu --set full --import-source on --clock-control none -k regex:advance_kernel \
-      --launch-skip 1 -c 1 -o gpurun_out/prof_adv_cfg1 -f \
-      python tools/prof_advance.py --pre 4000 --reps 1 > gpurun_out/ncu_adv1.log 2>&1
+      -c 1 -o gpurun_out/prof_adv_cfg1 -f \
+      python tools/prof_advance.py --steps 10000 --snap 1000 --reps 1 > gpurun_out/ncu_adv1.log 2>&1
 run adv2 python tools/prof_advance.py --config 2 --n 4194304 --pre 200 --reps 1 && \
   ncu --set full --import-source on --clock-control none -k regex:advance_kernel \
       --launch-skip 1 -c 1 -o gpurun_out/prof_adv_cfg2 -f \
