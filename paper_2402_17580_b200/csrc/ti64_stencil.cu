@@ -197,14 +197,13 @@ constexpr int RY = RY_DEF;
 #endif
 constexpr int TYT = TY * RY;  // tile height in cells
 
-template <bool COUPLED>
-__device__ __forceinline__ void cell_kinetics(ti64_fields& f, uint32_t* __restrict__ idle,
-                                              const CoupledODE& o, int lane, bool in,
-                                              int64_t flat, uint32_t bits, double t0,
-                                              double t_new, unsigned gm) {
-  const bool was_idle = in && ((bits >> lane) & 1u);
-  const bool rest = o.rest_ok && was_idle && t0 < o.kp.t_as_end && t_new < o.kp.t_as_end;
-  if (__all_sync(0xffffffffu, rest || !in)) return;
+// Kinetics of the warp's cells when at least one of them is not at rest:
+// out of line, so the stencil loop around the (usually taken) rest exit
+// keeps a small register footprint.
+static __device__ __noinline__ void cells_step(const ti64_fields& f, uint32_t* __restrict__ idle,
+                                               const CoupledODE& o, int lane, bool in,
+                                               bool rest, int64_t flat, uint32_t bits,
+                                               double t0, double t_new, unsigned gm) {
   bool touched = false;
   bool now_idle = rest;
   Seed sd;
@@ -236,10 +235,21 @@ __device__ __forceinline__ void cell_kinetics(ti64_fields& f, uint32_t* __restri
 }
 
 template <bool COUPLED>
+__device__ __forceinline__ void cell_kinetics(const ti64_fields& f, uint32_t* __restrict__ idle,
+                                              const CoupledODE& o, int lane, bool in,
+                                              int64_t flat, uint32_t bits, double t0,
+                                              double t_new, unsigned gm) {
+  const bool was_idle = in && ((bits >> lane) & 1u);
+  const bool rest = o.rest_ok && was_idle && t0 < o.kp.t_as_end && t_new < o.kp.t_as_end;
+  if (__all_sync(0xffffffffu, rest || !in)) return;  // warp-uniform exit
+  cells_step(f, idle, o, lane, in, rest, flat, bits, t0, t_new, gm);
+}
+
+template <bool COUPLED>
 __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
     const double* __restrict__ src, double* __restrict__ dst, ti64_stencil_args a,
-    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle,
-    const __grid_constant__ CoupledODE o) {
+    StencilConst c, int zchunk, const __grid_constant__ ti64_fields f,
+    uint32_t* __restrict__ idle, const __grid_constant__ CoupledODE o) {
   constexpr int W = TX + 2;              // smem row pitch
   constexpr int SLOT = (TYT + 2) * W;    // doubles per ring slot
   __shared__ double ring[RING * SLOT];
@@ -426,13 +436,13 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, uint64_t desc, int c0,
 #define TMA_MINB 4
 #endif
 #ifndef TMA_MINB_C
-#define TMA_MINB_C 1
+#define TMA_MINB_C 2
 #endif
 template <bool COUPLED>
 __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, double* __restrict__ dst, ti64_stencil_args a,
-    StencilConst c, int zchunk, ti64_fields f, uint32_t* __restrict__ idle,
-    const __grid_constant__ CoupledODE o) {
+    StencilConst c, int zchunk, const __grid_constant__ ti64_fields f,
+    uint32_t* __restrict__ idle, const __grid_constant__ CoupledODE o) {
   using T = TileOf<COUPLED>;
   constexpr int RY = T::RY, TYT = T::TYT, BOX_BYTES = T::BOX_BYTES, SLOT_BYTES = T::SLOT_BYTES;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -523,8 +533,7 @@ __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built
       cp_async_wait<PD>();
       __syncthreads();
     }
-    if (!COUPLED && xy_interior && z > 0 && z + 1 < nz &&
-        !(a.source_on != 0 && z == a.z_top - 1)) {
+    if (xy_interior && z > 0 && z + 1 < nz && !(a.source_on != 0 && z == a.z_top - 1)) {
       // interior plane of an interior tile: all six faces present, no source
       // or boundary value; same face order and association as below
       double* dz = dcol + (int64_t)z * plane;
@@ -538,7 +547,11 @@ __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built
         flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(P[W], t0)));
         flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sm * SLOTD + cidx[r]], t0)));
         flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sp1 * SLOTD + cidx[r]], t0)));
-        dz[(int64_t)yr[r] * nx] = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
+        const double t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
+        dz[(int64_t)yr[r] * nx] = t_new;
+        if (COUPLED)
+          cell_kinetics<COUPLED>(f, idle, o, lane, true, (int64_t)z * plane + (int64_t)yr[r] * nx + x,
+                                 iring[s0 * TYT + ty + r * TY], t0, t_new, gm);
       }
       __syncthreads();
       const int t = sm;
