@@ -45,6 +45,7 @@ _SIGS = {
     "ti64_phase_sums": (_I64, [_P, _P, _P, _I64, _P, _P, _P]),
     "ti64_histogram": (_I64, [_P, _P, _P, _I64, _I32, _P, _P]),
     "ti64_stencil_step": (_I64, [_P, _P, _P, _P, _P, _P, _P]),
+    "ti64_thermal_substeps": (_I64, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P]),
     "ti64_bench_dfma": (_I64, [_P, _I64, _I32, _P]),
     "ti64_bench_daxpy": (_I64, [_P, _P, _D, _I64, _P]),
     "ti64_coupled_step": (_I64, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _P]),

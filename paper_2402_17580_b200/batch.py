@@ -19,6 +19,7 @@ generators), ``phase_sums``, ``histogram``, ``run_history``.
 """
 
 import ctypes as C
+import functools
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -196,13 +197,23 @@ def _cfg(config):
     return _abi.icfg_from(config.kernel_tuple())
 
 
+@functools.lru_cache(maxsize=64)
+def _kp_struct(kp_tuple):
+    return _abi.kparams_from(kp_tuple)
+
+
+@functools.lru_cache(maxsize=64)
+def _cfg_struct(cfg_tuple):
+    return _abi.icfg_from(cfg_tuple)
+
+
 def run_range(fields, start, stop, lanes, nsub, dt_sub, kp_tuple, cfg_tuple,
               record_iters=False, iters_out=None, stream=None):
     """Kernel entry (batch.py:716-727): one macro step of points [start, stop)."""
     lib = _lib.require()
     fs = fields.cstruct()
-    kp = _abi.kparams_from(kp_tuple)
-    cfg = _abi.icfg_from(cfg_tuple)
+    kp = _kp_struct(kp_tuple)
+    cfg = _cfg_struct(cfg_tuple)
     rc = lib.ti64_run_range(C.byref(fs), int(start), int(stop), int(lanes), int(nsub),
                             float(dt_sub), C.byref(kp), C.byref(cfg), int(bool(record_iters)),
                             _lib.ptr(iters_out), _lib.stream_handle(stream))

@@ -806,3 +806,25 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   ti64_set_error("");
   return TI64_OK;
 }
+
+// _thermal_substeps (thermal.py:290-318): nsub stencil steps from src into
+// dst, intermediate results alternating through buf_a / buf_b, src left
+// untouched — one C call per macro step instead of one host round trip per
+// substep (the build's cool-down steps take up to ~1500 substeps each).
+extern "C" int64_t ti64_thermal_substeps(const double* src_d, double* dst_d, double* buf_a_d,
+                                         double* buf_b_d, double* rc_d, const uint8_t* state_d,
+                                         const ti64_thermal* tp, const ti64_stencil_args* a,
+                                         int64_t nsub, void* stream) {
+  if (nsub < 1 || (nsub > 1 && (!buf_a_d || (nsub > 2 && !buf_b_d)))) {
+    ti64_set_error("ti64_thermal_substeps: bad argument (nsub >= 1, scratch buffers)");
+    return TI64_EINVAL;
+  }
+  const double* cur = src_d;
+  for (int64_t s = 0; s < nsub; ++s) {
+    double* out = (s == nsub - 1) ? dst_d : ((s % 2 == 0) ? buf_a_d : buf_b_d);
+    const int64_t rc = ti64_stencil_step(cur, out, rc_d, state_d, tp, a, stream);
+    if (rc != TI64_OK) return rc;
+    cur = out;
+  }
+  return TI64_OK;
+}

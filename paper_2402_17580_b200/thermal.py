@@ -224,19 +224,21 @@ def step_thermal(field, dt, params=DEFAULT_THERMAL, source=None, beam=None, loss
                           all_built=all_built)
     tp = _abi.thermal_from(params.kernel_tuple())
     st = _lib.stream_handle(stream)
-    cur = field.temperature_old
-    bufs = [None, None]
-    for s in range(nsub):
-        if s == nsub - 1:
-            dst = field.temperature_new
-        else:
-            if bufs[s % 2] is None:
-                bufs[s % 2] = torch.empty_like(field.temperature_old)
-            dst = bufs[s % 2]
-        rc = lib.ti64_stencil_step(_lib.ptr(cur), _lib.ptr(dst), _lib.ptr(field.r_c),
+    if nsub == 1:
+        rc = lib.ti64_stencil_step(_lib.ptr(field.temperature_old),
+                                   _lib.ptr(field.temperature_new), _lib.ptr(field.r_c),
                                    _lib.ptr(field.state), C.byref(tp), C.byref(a), st)
         _lib.check(rc, "ti64_stencil_step")
-        cur = dst
+        return field
+    bufs = getattr(field, "_substep_bufs", None)
+    if bufs is None or bufs[0].shape != field.temperature_old.shape:
+        bufs = (torch.empty_like(field.temperature_old), torch.empty_like(field.temperature_old))
+        field._substep_bufs = bufs  # reused across macro steps (stream-ordered)
+    rc = lib.ti64_thermal_substeps(_lib.ptr(field.temperature_old),
+                                   _lib.ptr(field.temperature_new), _lib.ptr(bufs[0]),
+                                   _lib.ptr(bufs[1]), _lib.ptr(field.r_c), _lib.ptr(field.state),
+                                   C.byref(tp), C.byref(a), int(nsub), st)
+    _lib.check(rc, "ti64_thermal_substeps")
     return field
 
 
@@ -521,12 +523,17 @@ def run_build(geometry, scan_path, schedule=BuildSchedule(), thermal_params=DEFA
     counts = [0, 0]
     state_flat = field.state.view(-1)
 
+    prefix = {}  # the active z-prefix view changes only when a layer is activated
+
     def couple(dt, beam, bottom, phase):
         nonlocal t_now
         step_thermal(field, dt, thermal_params, source, beam, losses=True,
                      bottom_dirichlet=bottom, all_built=False)
         counts[0] += 1
-        step_all(_active_prefix(field, fields), dt, kp, cfg, n_lanes=n_lanes)
+        if field.z_top not in prefix:
+            prefix.clear()
+            prefix[field.z_top] = _active_prefix(field, fields)
+        step_all(prefix[field.z_top], dt, kp, cfg, n_lanes=n_lanes)
         counts[1] += 1
         t_now += dt
         if probe_hook is not None:
