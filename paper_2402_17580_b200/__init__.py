@@ -26,6 +26,8 @@ from .integrator import (
     SeedingState,
     integrate_history,
     integrate_interval,
+    initiate_diffusion,
+    analytic_beta_growth,
     step_crank_nicolson,
     wrms_norm,
     step_explicit,
@@ -60,7 +62,7 @@ __all__ = [
     "KineticsParams", "PhaseState", "DEFAULT_PARAMS", "X_ALPHA_MAX",
     "IntegratorConfig", "SeedingState",
     "step_explicit", "step_crank_nicolson", "integrate_interval", "integrate_history",
-    "FixedPointDivergence", "wrms_norm",
+    "FixedPointDivergence", "wrms_norm", "initiate_diffusion", "analytic_beta_growth",
     "GlobalFields", "step_all", "BatchConvergenceError", "SUPPORTED_LANES", "BYTES_PER_POINT",
     "advance", "AdvanceResult", "EventCounters", "phase_sums", "histogram",
     "init_from_source",

@@ -23,6 +23,7 @@ reference's own entry points:
   cn_steps.npz, cn_history.npz  Crank-Nicolson step_all / integrate_history
   acceptance.npz the reference's acceptance-criterion quantities
                  (test_acceptance.py), incl. the coupled cube builds
+  initiation.npz initiate_diffusion sequences (integrator.py:214-265)
   kinetics_api.npz  kinetics.py model functions + fastmath estrin/horner
   report.npz     bench.count_flops / RooflineReport text, output.py VTK
                  snapshots and probe CSV of a micro build
@@ -624,7 +625,35 @@ def make_acceptance():
     np.savez_compressed(OUT / "acceptance.npz", **c)
 
 
+def make_initiation():
+    """integrator.initiate_diffusion (integrator.py:214-265) sequences."""
+    from ti64micro.integrator import initiate_diffusion, SeedingState
+    from ti64micro.kinetics import PhaseState
+    c = {}
+    seqs = {"a2b_1200": (PhaseState(0.9, 0.0, 0.1), 1200.0, 1e-3, 400),
+            "a2b_1100_dt01": (PhaseState(0.9, 0.0, 0.1), 1100.0, 0.01, 300),
+            "b2a_1000": (PhaseState(0.0, 0.0, 1.0), 1000.0, 0.01, 50),
+            "b2a_900": (PhaseState(0.0, 0.0, 1.0), 900.0, 0.05, 80),
+            "melt_2000": (PhaseState(0.9, 0.0, 0.1), 2000.0, 1e-3, 3),
+            "cold_300": (PhaseState(0.9, 0.0, 0.1), 300.0, 1e-3, 3)}
+    for name, (st, t, dt, n) in seqs.items():
+        rows = []
+        seed = None
+        for _ in range(n):
+            st, seed = initiate_diffusion(st, t, dt, seed)
+            rows.append([st.x_alpha_s, st.x_alpha_m, st.x_beta, float(seed.active),
+                         {None: 0.0, "beta_to_alpha_s": 1.0, "alpha_s_to_beta": 2.0}[seed.direction],
+                         seed.tracked])
+        c[f"{name}/rows"] = np.array(rows)
+        c[f"{name}/args"] = np.array([t, dt, n])
+    np.savez_compressed(OUT / "initiation.npz", **c)
+
+
 if __name__ == "__main__":
+    if "--init-only" in sys.argv:
+        make_initiation()
+        print("initiation done")
+        sys.exit(0)
     if "--acceptance-only" in sys.argv:
         make_acceptance()
         print("acceptance done")
@@ -655,6 +684,8 @@ if __name__ == "__main__":
     print("kinetics api done")
     make_acceptance()
     print("acceptance done")
+    make_initiation()
+    print("initiation done")
     make_fastmath()
     print("fastmath done")
     make_steps()
