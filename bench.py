@@ -319,6 +319,13 @@ def measure_extra(torch, pkg, dev):
                                         "cell_steps_per_s": n / t,
                                         "job_estimate_s": 20000 * t}
     del dom
+    # config 0 at its full size (4096 points x 20 000 steps, one launch)
+    src0 = pkg.source_for_config(0)
+    f0 = pkg.init_from_source(src0, 4096, device=dev)
+    pkg.advance(f0.copy(), 20000, src0, snapshot_every=1000)
+    t = _time_dev(torch, lambda: pkg.advance(f0.copy(), 20000, src0, snapshot_every=1000), 3)
+    out["config0_full_4096x20000"] = {"point_updates_per_s": 4096 * 20000 / t, "ms": t * 1e3,
+                                      "note": "128 warps on 148 SMs: latency-bound by size"}
     for c in (2, 4):
         src_c = pkg.source_for_config(c)
         f = pkg.init_from_source(src_c, 1 << 22, device=dev)
