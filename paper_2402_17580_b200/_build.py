@@ -24,7 +24,7 @@ HEADERS = ["ti64_fastmath.cuh", "ti64_point.cuh", "ti64_sources.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-Xcompiler", "-ffp-contract=off",
     "-Xptxas", "-O3",
 ]
 
