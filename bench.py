@@ -37,8 +37,8 @@ UNIT = "point-updates/s"
 JOB_STEPS = 10_000
 SNAP_EVERY = int(os.environ.get("TI64_BENCH_SNAP", "1000"))  # snapshot interval (steps)
 # DRAM bytes (read + write) of the job's single K2 launch, from the committed
-# ncu capture profiles/r01_advance_cfg1_job.txt (44.87 MB + 8.89 MB)
-K2_JOB_DRAM_BYTES = 44_866_816 + 8_892_160
+# ncu capture profiles/r01b_advance_cfg1_job.txt (44.53 MB + 9.56 MB)
+K2_JOB_DRAM_BYTES = 44_533_248 + 9_556_736
 WORKLOAD = ("config1: Rosenthal raster (200 W, eta 0.35, 1 m/s, 100 um hatch), "
             "N=2^20 points on 128x128x64 lattice h=20um, 10000 steps dt=2e-5 s, "
             "state (0.9,0,0.1)")
@@ -284,8 +284,9 @@ def _time_dev(torch, fn, reps=5, flush=None):
 
 def measure_extra(torch, pkg, dev):
     """Secondary evidence (not the headline): the HBM-bound stencil K4 and the
-    fused config-3 step at 512x512x256, and the all-active pure-ODE configs 2
-    and 4 on a 2^22-point shard for 2000 steps (per-GPU, fp64)."""
+    fused config-3 step at 512x512x256, config 0 at full size, mid-job
+    windows of the all-active pure-ODE configs 2 and 4 with their FP64
+    roofline, and the Crank-Nicolson step_all (per-GPU, fp64)."""
     from paper_2402_17580_b200 import thermal as th, scanpath
     hbm = 6538.0
     try:
@@ -331,13 +332,26 @@ def measure_extra(torch, pkg, dev):
     t = _time_dev(torch, lambda: pkg.advance(f0.copy(), 20000, src0, snapshot_every=1000), 3)
     out["config0_full_4096x20000"] = {"point_updates_per_s": 4096 * 20000 / t, "ms": t * 1e3,
                                       "note": "128 warps on 148 SMs: latency-bound by size"}
-    for c in (2, 4):
+    # the all-active pure-ODE configs: a mid-job window of 2000 steps on a
+    # per-GPU shard, from the state the job has reached there (config 2 at
+    # step 10 000 of 50 000 with 2^22 points, config 4 at step 50 000 of
+    # 100 000 with 2^21 points); every point transforms every step.  F from
+    # one counted run of the same window (the headline's flop model).
+    for c, nsh, s0 in ((2, 1 << 22, 10000), (4, 1 << 21, 50000)):
         src_c = pkg.source_for_config(c)
-        f = pkg.init_from_source(src_c, 1 << 22, device=dev)
-        pkg.advance(f, 200, src_c, snapshot_every=1000)
-        t = _time_dev(torch, lambda: pkg.advance(f.copy(), 2000, src_c, step0=200,
-                                                snapshot_every=1000), 1)
-        out[f"config{c}_shard_2^22x2000"] = {"point_updates_per_s": (1 << 22) * 2000 / t}
+        f = pkg.init_from_source(src_c, nsh, device=dev)
+        pkg.advance(f, s0, src_c)
+        cnt = pkg.EventCounters(nsh, dev)
+        pkg.advance(f.copy(), 2000, src_c, step0=s0, counters=cnt)
+        fl = flops_from_totals(cnt.totals_dict())
+        t = _time_dev(torch, lambda: pkg.advance(f.copy(), 2000, src_c, step0=s0), 3)
+        rate = nsh * 2000 / t
+        out[f"config{c}_shard_2^{nsh.bit_length() - 1}_steps_{s0}-{s0 + 2000}"] = {
+            "point_updates_per_s": rate, "ms": t * 1e3,
+            "flops_per_update": fl / (nsh * 2000), "TFLOP/s": fl / t / 1e12,
+            "job_estimate_s_per_gpu": {2: (1 << 24) * 50000, 4: (1 << 24) * 100000}[c] / rate,
+            "job_note": "config 2: full 2^24-point job on one GPU; config 4: the 2^24-point "
+                        "per-GPU shard of the 8-GPU job"}
     # Crank-Nicolson step_all on the reference's block-100 benchmark layout
     # (bench.py:131-155: dt = dt_sub_max = 0.01), its analytic flop count
     cfg = pkg.IntegratorConfig(scheme="crank_nicolson", dt_sub_max=0.01)
@@ -492,9 +506,9 @@ def run_b200(args):
         flops_launch = flops_job / adv_per_job
         achieved = flops_launch / per_launch_s / 1e12
         peak_tf = peak / 1e12
-        cn = (extra or {}).get("crank_nicolson_layout_block100_2^22")
-        if cn:
-            cn["frac_of_fp64_peak"] = cn["TFLOP/s"] / peak_tf
+        for v in (extra or {}).values():
+            if isinstance(v, dict) and "TFLOP/s" in v:
+                v["frac_of_fp64_peak"] = v["TFLOP/s"] / peak_tf
         cpu = None if args.no_cpu_baseline else cpu_reference(budget_s=args.cpu_budget)
         clocks = clk.summary()
         line = {
@@ -510,7 +524,7 @@ def run_b200(args):
                          "unit": "TFLOP/s", "frac": achieved / peak_tf,
                          "traffic": K2_JOB_DRAM_BYTES,
                          "traffic_source": "ncu --set full of this job's K2 launch "
-                                           "(profiles/r01_advance_cfg1_job.txt): "
+                                           "(profiles/r01b_advance_cfg1_job.txt): "
                                            "dram read + write bytes per launch",
                          "peak_source": "measured on this box: DFMA stream (ti64_bench_dfma)",
                          "flops_per_update": flops_job / upd_job,
