@@ -32,3 +32,8 @@ print("$v", "cfg1 ms/job", round(d["ms_per_step"], 2), "cfg2/cfg4 active G upd/s
 PY
   done
 done
+# single-task step latency of config 1 (the 32 surface points 0..31 alone)
+for v in "$@"; do
+  echo -n "$v cfg1 single task: "
+  TI64_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python tools/prof_advance.py --config 1 --n 32 --steps 10000 --reps 3 | tail -1
+done
