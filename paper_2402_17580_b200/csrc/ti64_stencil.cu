@@ -168,7 +168,7 @@ struct CoupledODE {
 // Each T_n value is read from HBM once per step (plus tile halos, L2 hits).
 // ---------------------------------------------------------------------------
 #ifndef PD_DEF
-#define PD_DEF 2
+#define PD_DEF 5
 #endif
 #ifndef RY_DEF
 #define RY_DEF 2
@@ -433,7 +433,7 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, uint64_t desc, int c0,
 }
 
 #ifndef TMA_MINB
-#define TMA_MINB 4
+#define TMA_MINB 3
 #endif
 #ifndef TMA_MINB_C
 #define TMA_MINB_C 2
