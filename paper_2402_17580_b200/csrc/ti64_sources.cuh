@@ -232,8 +232,9 @@ struct Rosenthal {
   }
 
   // exact T at the step rows (bfp float row, b double row)
+  template <class C = CoefBank>
   __device__ __forceinline__ double temp(const float4* bfp, const double* b,
-                                         const ti64_tempgen& g) const {
+                                         const ti64_tempgen& g, const C& cf = C()) const {
     {
       // no-op filter: vk (R + xi) > arg_noop  <=>  R > c := arg_noop/vk - xi
       const float4 bf = __ldg(bfp);
@@ -251,7 +252,7 @@ struct Rosenthal {
     if (arg > 708.0) {
       tt = g.base;  // fast_exp == 0 exactly; (coef/r)*0 == +0 (r > 0 here)
     } else {
-      tt = __dadd_rn(g.base, __dmul_rn(__ddiv_rn(g.p[0], r), exp_core(-arg)));
+      tt = __dadd_rn(g.base, __dmul_rn(__ddiv_rn(g.p[0], r), exp_core(-arg, cf)));
     }
     return tt > g.p[2] ? g.p[2] : tt;
   }
