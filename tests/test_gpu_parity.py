@@ -250,6 +250,41 @@ def test_advance_cfg1_full_lattice_block_vs_oracle(pkg, orc):
             assert_bitwise(h[k][off:off + 4096], getattr(ho, k), f"block {off}:{k}")
 
 
+@pytest.mark.parametrize("cfg_id,step0,nsteps", [(0, 2000, 1500), (2, 2000, 1200), (4, 0, 1200)])
+def test_advance_pulse_throughput_instance_vs_oracle(pkg, orc, cfg_id, step0, nsteps):
+    """Pulse generators at a launch size that takes the throughput instance
+    of K2 (72 registers; small launches take the latency instance, which the
+    golden tests cover): two 2048-point blocks checked by the oracle bit for
+    bit, and the whole launch equal to the same points run as small
+    (latency-instance) launches."""
+    from paper_2402_17580_b200.batch import gen_temperature
+    src = pkg.source_for_config(cfg_id)
+    n = 1 << 16
+    f = pkg.init_from_source(src, n)
+    if step0:
+        f.temperature_old.copy_(gen_temperature(src, n, step0))
+    pkg.advance(f, nsteps, src, step0=step0, snapshot_every=500)
+    h = f.to_host()
+    kp = pkg.DEFAULT_PARAMS.kernel_tuple()
+    cfg = pkg.IntegratorConfig().kernel_tuple()
+    for off in (0, n - 2048):
+        g = src.tempgen(point_offset=off)
+        ho = orc.gen_initial_state(g, 2048)
+        t0 = orc.gen_temperature(g, 2048, step0)
+        ho.temperature_old[:] = t0
+        ho.temperature_new[:] = t0
+        orc.advance(ho, g, step0, nsteps, kp, cfg, lanes=8, threads=8)
+        for k in FIELD_NAMES:
+            assert_bitwise(h[k][off:off + 2048], getattr(ho, k), f"cfg{cfg_id} block {off}:{k}")
+    small = pkg.init_from_source(src, 4096, point_offset=8192)
+    if step0:
+        small.temperature_old.copy_(gen_temperature(src, 4096, step0, point_offset=8192))
+    pkg.advance(small, nsteps, src, step0=step0, snapshot_every=500, point_offset=8192)
+    hs = small.to_host()
+    for k in FIELD_NAMES:
+        assert_bitwise(h[k][8192:8192 + 4096], hs[k], f"cfg{cfg_id} lat-vs-throughput:{k}")
+
+
 def test_full_config1_invariants(pkg):
     """Size-independent properties at BASELINE config 1's full size and
     length: continuity sum == 1 - g(T) (acceptance criterion 3, <= 1e-12),
