@@ -42,6 +42,7 @@ _SIGS = {
     "ti64_fast_exp": (_I64, [_P, _P, _I64, _P]),
     "ti64_fast_ln": (_I64, [_P, _P, _I64, _P]),
     "ti64_fast_pow": (_I64, [_P, _P, _P, _I64, _P]),
+    "ti64_div_rn": (_I64, [_P, _P, _P, _P, _I64, _P]),
     "ti64_phase_sums": (_I64, [_P, _P, _P, _I64, _P, _P, _P]),
     "ti64_histogram": (_I64, [_P, _P, _P, _I64, _I32, _P, _P]),
     "ti64_stencil_step": (_I64, [_P, _P, _P, _P, _P, _P, _P]),

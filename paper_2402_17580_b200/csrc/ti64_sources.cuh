@@ -74,7 +74,7 @@ struct PulseSet {
   __device__ __forceinline__ void add(int k, double ak, double tck, double w, double dt) {
     a[k] = ak;
     tc[k] = tck;
-    inv_w[k] = __ddiv_rn(1.0, w);
+    inv_w[k] = div_rn(1.0, w);
     // conservative window: outside it |t - tc| >= 7w - O(ulp) => u^2 > 45
     const double l = floor((tck - 7.0 * w) / dt) - 2.0;
     const double h = ceil((tck + 7.0 * w) / dt) + 2.0;
@@ -252,7 +252,7 @@ struct Rosenthal {
     if (arg > 708.0) {
       tt = g.base;  // fast_exp == 0 exactly; (coef/r)*0 == +0 (r > 0 here)
     } else {
-      tt = __dadd_rn(g.base, __dmul_rn(__ddiv_rn(g.p[0], r), exp_core(-arg, cf)));
+      tt = __dadd_rn(g.base, __dmul_rn(div_rn(g.p[0], r), exp_core(-arg, cf)));
     }
     return tt > g.p[2] ? g.p[2] : tt;
   }

@@ -214,6 +214,95 @@ def test_advance_equals_step_loop(pkg, cfg_id, nsteps, lanes):
         assert_bitwise(ha[k], hb[k], f"cfg{cfg_id}:{k}")
 
 
+@pytest.mark.parametrize("cfg_id,n", [(0, 8192 + 13), (1, 4096), (2, 1 << 16)])
+def test_advance_subcycled_equals_step_loop(pkg, cfg_id, n):
+    """nsub > 1 (dt_sub_max = dt / 2.5 -> 3 substeps with interpolated T):
+    the general K2 instances (counted and uncounted) == the step_all loop."""
+    from paper_2402_17580_b200.batch import gen_temperature
+    src = pkg.source_for_config(cfg_id)
+    if cfg_id == 1:
+        src = pkg.RosenthalRaster(nx=64, ny=64, nz=1)
+    config = pkg.IntegratorConfig(dt_sub_max=src.dt / 2.5)
+    step0 = 2000 if cfg_id in (0, 2) else 0
+    nsteps = 300
+    a = pkg.init_from_source(src, n)
+    if step0:
+        a.temperature_old.copy_(gen_temperature(src, n, step0))
+    b, c = a.copy(), a.copy()
+    pkg.advance(a, nsteps, src, step0=step0, config=config)
+    pkg.advance(c, nsteps, src, step0=step0, config=config, counters=pkg.EventCounters(n, c.device))
+    for st in range(step0, step0 + nsteps):
+        b.temperature_new.copy_(gen_temperature(src, n, st + 1))
+        pkg.step_all(b, src.dt, config=config)
+    ha, hb, hc = a.to_host(), b.to_host(), c.to_host()
+    for k in FIELD_NAMES:
+        if k == "temperature_new":
+            continue
+        assert_bitwise(ha[k], hb[k], f"cfg{cfg_id} nsub3:{k}")
+        assert_bitwise(hc[k], hb[k], f"cfg{cfg_id} nsub3 counted:{k}")
+
+
+def test_div_rn(pkg):
+    """div_rn (the kinetics' inline division) == __ddiv_rn bit for bit: random
+    bit patterns over the whole range (subnormal operands and quotients,
+    overflow, specials) and quotients straddling the subnormal threshold."""
+    import torch
+    from paper_2402_17580_b200 import _lib
+    lib = _lib.require()
+    rng = np.random.default_rng(7)
+    n = 1 << 22
+    a = rng.integers(0, 2**64, n, dtype=np.uint64).view(np.float64).copy()
+    b = rng.integers(0, 2**64, n, dtype=np.uint64).view(np.float64).copy()
+    # quotients near and below the smallest normal, and near overflow
+    m = n // 4
+    b[:m] = rng.uniform(1.0, 2.0, m) * 2.0 ** rng.integers(-60, 60, m)
+    a[:m] = b[:m] * rng.uniform(0.5, 2.0, m) * 2.0 ** rng.integers(-1080, -1015, m).astype(float)
+    a[m:2 * m] = rng.uniform(1.0, 2.0, m) * 2.0 ** rng.integers(-1074, 1024, m).astype(float)
+    b[m:2 * m] = rng.uniform(1.0, 2.0, m) * 2.0 ** rng.integers(-1074, 1024, m).astype(float)
+    # exact ties into the subnormal range: odd multiples of 2^-1075 times b
+    k = rng.integers(1, 2**20, 4096) * 2 + 1
+    bb = rng.integers(1, 2**20, 4096).astype(float)
+    a[2 * m:2 * m + 4096] = np.ldexp(k * bb, -1075)
+    b[2 * m:2 * m + 4096] = bb
+    specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, -1.0, 5e-324, 2.2250738585072014e-308,
+                         1.7976931348623157e308, 3.0, 1e-300, 1e300])
+    sa, sb = np.meshgrid(specials, specials)
+    a[-sa.size:] = sa.ravel()
+    b[-sb.size:] = sb.ravel()
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    out, ref = torch.empty_like(da), torch.empty_like(da)
+    rc = lib.ti64_div_rn(_lib.ptr(da), _lib.ptr(db), _lib.ptr(out), _lib.ptr(ref), n, None)
+    assert rc == 0
+    o, r = out.cpu().numpy(), ref.cpu().numpy()
+    assert_bitwise(o, r, "div_rn vs __ddiv_rn")
+    # and the host's IEEE division (the reference's numba divsd) on non-NaN results
+    with np.errstate(all="ignore"):
+        h = a / b
+    ok = ~np.isnan(h)
+    assert_bitwise(o[ok], h[ok], "div_rn vs host IEEE")
+
+
+def test_k1_subcycled_seed_warp_regression(pkg, orc):
+    """One warp of config 2's state at step 2026 (points 96-127 of a 2^16
+    run; two lanes with an active seed, the others on the rate path), stepped
+    with nsub = 3: with seed_advance as an out-of-line call this warp faulted
+    (illegal address) or hung on sm_100a.  The fixture is our own state dump
+    (tests/golden/k1_nsub3_seed_warp.npz), checked against the oracle."""
+    g = load_golden("k1_nsub3_seed_warp.npz")
+    names = ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old", "temperature_new")
+    dt = 1e-5
+    config = pkg.IntegratorConfig(dt_sub_max=dt / 2.5)
+    f = pkg.GlobalFields(*[g[k] for k in names], seed_tracked=g["seed_tracked"],
+                         seed_active=g["seed_active"], seed_direction=g["seed_direction"])
+    h = orc.HostFields(*[g[k] for k in names], seed_tracked=g["seed_tracked"],
+                       seed_active=g["seed_active"], seed_direction=g["seed_direction"])
+    pkg.step_all(f, dt, config=config)
+    orc.step_all(h, dt, pkg.DEFAULT_PARAMS.kernel_tuple(), config.kernel_tuple(), n_lanes=8)
+    got = f.to_host()
+    for k in FIELD_NAMES:
+        assert_bitwise(got[k], getattr(h, k), f"seed warp nsub3:{k}")
+
+
 def test_generator_matches_oracle(pkg, orc):
     from paper_2402_17580_b200.batch import gen_temperature
     for cfg_id in (0, 1, 2, 4):
