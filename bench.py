@@ -37,8 +37,8 @@ UNIT = "point-updates/s"
 JOB_STEPS = 10_000
 SNAP_EVERY = int(os.environ.get("TI64_BENCH_SNAP", "1000"))  # snapshot interval (steps)
 # DRAM bytes (read + write) of the job's single K2 launch, from the committed
-# ncu capture profiles/r01b_advance_cfg1_job.txt (44.64 MB + 9.29 MB)
-K2_JOB_DRAM_BYTES = 44_638_208 + 9_292_032
+# ncu capture profiles/r01b_advance_cfg1_job.txt (44.59 MB + 7.66 MB)
+K2_JOB_DRAM_BYTES = 44_589_568 + 7_659_776
 WORKLOAD = ("config1: Rosenthal raster (200 W, eta 0.35, 1 m/s, 100 um hatch), "
             "N=2^20 points on 128x128x64 lattice h=20um, 10000 steps dt=2e-5 s, "
             "state (0.9,0,0.1)")
