@@ -1,5 +1,6 @@
 """Config-3 determinism: the fused coupled run (512x512x256, 3000 steps) twice
 from the same start, every state array compared bit for bit."""
+import sys
 sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_2402_17580_b200 as pkg
