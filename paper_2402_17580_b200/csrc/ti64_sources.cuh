@@ -13,6 +13,10 @@
 #include "ti64_fastmath.cuh"
 #include "../../include/ti64_b200.h"
 
+#ifndef PULSE_CACHE
+#define PULSE_CACHE 1
+#endif
+
 namespace ti64 {
 
 __host__ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
@@ -70,6 +74,11 @@ struct PulseSet {
   int np;
   unsigned live;
   int64_t next_event;
+#if PULSE_CACHE
+  // the lowest live pulse (the first term of the sum) in registers: usually
+  // the only live one, so the per-step sum needs no local-memory loads
+  double ca, ctc, ciw;
+#endif
 
   __device__ __forceinline__ void add(int k, double ak, double tck, double w, double dt) {
     a[k] = ak;
@@ -94,6 +103,14 @@ struct PulseSet {
       }
     }
     next_event = nxt;
+#if PULSE_CACHE
+    if (live) {
+      const int k = __ffs(live) - 1;
+      ca = a[k];
+      ctc = tc[k];
+      ciw = inv_w[k];
+    }
+#endif
   }
 
   // FP32 estimate of T - base (relative error < 1e-5; u is formed in FP64
@@ -104,6 +121,13 @@ struct PulseSet {
     if (m == 0u) return 0.0f;
     const double t = __dmul_rn(step_to_double(n), dt);
     float e = 0.0f;
+#if PULSE_CACHE
+    {
+      const float u = (float)__dmul_rn(__dsub_rn(t, ctc), ciw);
+      e += (float)ca * exp2f_approx(-u * u * 1.44269504f);
+      m &= m - 1;
+    }
+#endif
     while (m) {
       const int k = __ffs(m) - 1;
       m &= m - 1;
@@ -119,6 +143,10 @@ struct PulseSet {
     unsigned m = live;
     if (m == 0u) return s;  // every pulse is an exact no-op: T == base
     const double t = __dmul_rn(step_to_double(n), dt);
+#if PULSE_CACHE
+    s = add_pulse(s, ca, ctc, ciw, t);
+    m &= m - 1;
+#endif
     while (m) {
       const int k = __ffs(m) - 1;
       m &= m - 1;
