@@ -19,6 +19,7 @@
 #include <cuda.h>  // CUtensorMap (types only; the encoder comes via cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -155,6 +156,7 @@ struct CoupledODE {
   double dt;
   int L;
   int rest_ok;  // t_as_end <= t_sol etc.: the cold idle rest is exact
+  uint32_t* hot;  // split mode: 1 bit per 32-cell row, set where T_n or T_n+1 >= t_as_end
 };
 
 // ---------------------------------------------------------------------------
@@ -234,15 +236,108 @@ static __device__ __noinline__ void cells_step(const ti64_fields& f, uint32_t* _
   if (lane == 0 && nb != bits) idle[(flat - lane) >> 5] = nb;
 }
 
-template <bool COUPLED>
+// CM: 1 = fused (the kinetics of the warp's cells run here), 2 = split (the
+// stencil only marks rows with a hot cell; rows_kinetics_kernel runs next)
+template <int CM>
 __device__ __forceinline__ void cell_kinetics(const ti64_fields& f, uint32_t* __restrict__ idle,
                                               const CoupledODE& o, int lane, bool in,
                                               int64_t flat, uint32_t bits, double t0,
                                               double t_new, unsigned gm) {
-  const bool was_idle = in && ((bits >> lane) & 1u);
-  const bool rest = o.rest_ok && was_idle && t0 < o.kp.t_as_end && t_new < o.kp.t_as_end;
-  if (__all_sync(0xffffffffu, rest || !in)) return;  // warp-uniform exit
-  cells_step(f, idle, o, lane, in, rest, flat, bits, t0, t_new, gm);
+  if constexpr (CM == 2) {
+    // not provably cold (NaN included): the row's kinetics must run
+    // Integer screen on the high words (ALU pipe; the stencil's FP64 pipe is
+    // the busy one): |T| < t_as_end whenever hi(|T|) < hi(t_as_end), so a
+    // cell that is not flagged has T_n, T_n+1 < t_as_end; cells just below
+    // the bound and NaNs of either sign are flagged, and the kinetics kernel
+    // applies the exact test.  No vote: hot cells are rare and a warp's
+    // same-word atomics combine.
+    const int thi = __double2hiint(o.kp.t_as_end);
+    const int h = max(__double2hiint(t0) & 0x7fffffff, __double2hiint(t_new) & 0x7fffffff);
+    if (in && h >= thi) {
+      const int64_t row = flat >> 5;
+      atomicOr(o.hot + (row >> 5), 1u << (row & 31));
+    }
+  } else {
+    const bool was_idle = in && ((bits >> lane) & 1u);
+    const bool rest = o.rest_ok && was_idle && t0 < o.kp.t_as_end && t_new < o.kp.t_as_end;
+    if (__all_sync(0xffffffffu, rest || !in)) return;  // warp-uniform exit
+    cells_step(f, idle, o, lane, in, rest, flat, bits, t0, t_new, gm);
+  }
+}
+
+// Split coupled step, second half.  A 32-cell row (rows are whole: nx % 32
+// == 0) can skip its kinetics only if every cell is at the cold idle rest:
+// idle bit set and T_n, T_n+1 < t_as_end.  So a row runs iff its idle word
+// has a zero bit (transformed material, persistent) or the stencil marked it
+// hot.  rows_scan_kernel lists those rows (each thread reads 4 idle words as
+// one 16-byte load: the 1-bit/cell map is 1/64 of the temperature bytes) and
+// clears the hot bits; rows_kinetics_kernel runs one listed row per warp with
+// the fused kernel's rest test and cells_step on T_n (tn, untouched by the
+// stencil) and T_n+1 (tn1).  Rows are independent: list order is irrelevant.
+__global__ void __launch_bounds__(256) rows_scan_kernel(const uint32_t* __restrict__ idle,
+                                                        uint32_t* __restrict__ hot,
+                                                        int64_t nrows, uint32_t* __restrict__ list,
+                                                        unsigned int* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r0 = 4 * i;  // rows r0 .. r0+3 (nrows % 4 == 0 is not assumed)
+  unsigned m = 0u;
+  uint32_t hw = 0u;
+  if (r0 < nrows) {
+    hw = hot[r0 >> 5];
+    uint32_t v[4];
+    if (r0 + 4 <= nrows && (nrows & 3) == 0 && (reinterpret_cast<uintptr_t>(idle) & 15) == 0) {
+      const uint4 q = reinterpret_cast<const uint4*>(idle)[i];
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = r0 + k < nrows ? idle[r0 + k] : 0xffffffffu;
+    }
+    m = (hw >> (r0 & 31)) & 0xfu;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m |= (v[k] != 0xffffffffu ? 1u : 0u) << k;
+  }
+  // the 8 threads sharing a hot word are lanes of one warp: read, then clear
+  __syncwarp();
+  if (r0 < nrows && (r0 & 31) == 0 && hw) hot[r0 >> 5] = 0u;
+  const unsigned c = __popc(m);
+  unsigned pre = c;  // inclusive warp scan
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, pre, d);
+    if (lane >= d) pre += t;
+  }
+  const unsigned tot = __shfl_sync(0xffffffffu, pre, 31);
+  unsigned base = 0u;
+  if (lane == 31 && tot) base = atomicAdd(count, tot);
+  base = __shfl_sync(0xffffffffu, base, 31) + pre - c;
+  while (m) {
+    const int k = __ffs(m) - 1;
+    m &= m - 1;
+    list[base++] = (uint32_t)(r0 + k);
+  }
+}
+
+__global__ void __launch_bounds__(128) rows_kinetics_kernel(const double* __restrict__ tn,
+                                                            const double* __restrict__ tn1,
+                                                            const __grid_constant__ ti64_fields f,
+                                                            uint32_t* __restrict__ idle,
+                                                            const __grid_constant__ CoupledODE o,
+                                                            const uint32_t* __restrict__ list,
+                                                            const unsigned int* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const unsigned gm = ((o.L >= 32) ? 0xffffffffu : ((1u << o.L) - 1u)) << (lane & ~(o.L - 1));
+  const unsigned cnt = *count;
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < cnt; w += nw) {
+    const int64_t row = list[w];
+    const int64_t flat = row * 32 + lane;
+    const uint32_t bits = idle[row];
+    const double t0 = tn[flat], t_new = tn1[flat];
+    const bool rest = o.rest_ok && ((bits >> lane) & 1u) && t0 < o.kp.t_as_end &&
+                      t_new < o.kp.t_as_end;
+    cells_step(f, idle, o, lane, true, rest, flat, bits, t0, t_new, gm);
+  }
 }
 
 template <bool COUPLED>
@@ -340,7 +435,7 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
           dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
         }
         if (COUPLED)
-          cell_kinetics<COUPLED>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
+          cell_kinetics<COUPLED ? 1 : 0>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
                                  iring[s0 * TYT + ty + r * TY], t0, t_new, gm);
       }
     }
@@ -383,8 +478,8 @@ struct TmaTile {
   static constexpr int SLOT_BYTES = (BOX_BYTES + 127) / 128 * 128;
   static constexpr int SMEM = RING * SLOT_BYTES + RING * 8 + RING * TYT * 4;
 };
-template <bool COUPLED>
-using TileOf = TmaTile<COUPLED ? RY_C_DEF : RY_S_DEF>;
+template <int CM>
+using TileOf = TmaTile<CM == 1 ? RY_C_DEF : RY_S_DEF>;
 
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -438,12 +533,13 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, uint64_t desc, int c0,
 #ifndef TMA_MINB_C
 #define TMA_MINB_C 2
 #endif
-template <bool COUPLED>
-__global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built_tma_kernel(
+template <int CM>
+__global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, double* __restrict__ dst, ti64_stencil_args a,
     StencilConst c, int zchunk, const __grid_constant__ ti64_fields f,
     uint32_t* __restrict__ idle, const __grid_constant__ CoupledODE o) {
-  using T = TileOf<COUPLED>;
+  constexpr bool COUPLED = CM != 0;
+  using T = TileOf<CM>;
   constexpr int RY = T::RY, TYT = T::TYT, BOX_BYTES = T::BOX_BYTES, SLOT_BYTES = T::SLOT_BYTES;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);  // RING slots of SLOT_BYTES
@@ -493,7 +589,7 @@ __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built
       tma_load_3d(rbase + (unsigned)(slot * SLOT_BYTES), desc, x0 - 2, ybase - 1,
                   zz - (int)a.z_base, bar);
     }
-    if (COUPLED) {
+    if (CM == 1) {
       if (lane == 0 && zz >= z0 && zz < z1) {
 #pragma unroll
         for (int r = 0; r < RY; ++r)
@@ -529,7 +625,7 @@ __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built
   for (int z = z0; z < z1; ++z) {
     issue(z + 1 + PD, si);
     wait_plane(z + 1, sp1);
-    if (COUPLED) {
+    if (CM == 1) {
       cp_async_wait<PD>();
       __syncthreads();
     }
@@ -550,8 +646,8 @@ __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built
         const double t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
         dz[(int64_t)yr[r] * nx] = t_new;
         if (COUPLED)
-          cell_kinetics<COUPLED>(f, idle, o, lane, true, (int64_t)z * plane + (int64_t)yr[r] * nx + x,
-                                 iring[s0 * TYT + ty + r * TY], t0, t_new, gm);
+          cell_kinetics<CM>(f, idle, o, lane, true, (int64_t)z * plane + (int64_t)yr[r] * nx + x,
+                                 CM == 1 ? iring[s0 * TYT + ty + r * TY] : 0u, t0, t_new, gm);
       }
       __syncthreads();
       const int t = sm;
@@ -586,8 +682,8 @@ __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built
           dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
         }
         if (COUPLED)
-          cell_kinetics<COUPLED>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
-                                 iring[s0 * TYT + ty + r * TY], t0, t_new, gm);
+          cell_kinetics<CM>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
+                                 CM == 1 ? iring[s0 * TYT + ty + r * TY] : 0u, t0, t_new, gm);
       }
     }
     (void)tm_;
@@ -598,7 +694,7 @@ __global__ void __launch_bounds__(TX* TY, COUPLED ? TMA_MINB_C : TMA_MINB) built
     sp1 = (sp1 + 1 == RING) ? 0 : sp1 + 1;
     si = t;
   }
-  if (COUPLED) cp_async_wait<0>();
+  if (CM == 1) cp_async_wait<0>();
 }
 
 // --- host: tensor-map encoder through the runtime's driver entry point ----
@@ -644,11 +740,11 @@ bool make_plane_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, 
 
 // TMA launch: false when the grid cannot be mapped (callers fall back to the
 // cp.async kernel); the grid's y extent follows the kernel's own tile height
-template <bool COUPLED>
+template <int CM>
 bool launch_built(const double* src, double* dst, const ti64_stencil_args& a,
                   const StencilConst& c, ti64_fields f, uint32_t* idle, const CoupledODE& o,
                   int64_t nz_units, int zchunk, cudaStream_t st) {
-  using T = TileOf<COUPLED>;
+  using T = TileOf<CM>;
   CUtensorMap m;
   if (!make_plane_map(&m, src, a.nx, a.ny, a.nz_stored, T::BOX_Y)) return false;
   // the opt-in shared-memory size is a per-device function attribute
@@ -657,13 +753,13 @@ bool launch_built(const double* src, double* dst, const ti64_stencil_args& a,
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
-    cudaFuncSetAttribute(built_tma_kernel<COUPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(built_tma_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          T::SMEM);
     attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   dim3 grid((unsigned)((a.nx + TX - 1) / TX), (unsigned)((a.ny + T::TYT - 1) / T::TYT),
             (unsigned)((nz_units + zchunk - 1) / zchunk));
-  built_tma_kernel<COUPLED><<<grid, dim3(TX, TY), T::SMEM, st>>>(m, dst, a, c, zchunk, f, idle, o);
+  built_tma_kernel<CM><<<grid, dim3(TX, TY), T::SMEM, st>>>(m, dst, a, c, zchunk, f, idle, o);
   return true;
 }
 
@@ -692,6 +788,51 @@ bool use_tma() {
     v = (e && e[0] == '1') ? 0 : 1;
   }
   return v == 1;
+}
+// coupled-step mode: split (default: stencil marking hot rows in a bitmap, then
+// the kinetics of flagged and transformed rows) or fused (TI64_COUPLED_FUSED=1: the kinetics
+// inside the stencil kernel)
+bool coupled_split() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TI64_COUPLED_FUSED");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+// per-device scratch of the split coupled step: the hot-row bitmap (zeroed at
+// allocation, then word by word by rows_scan_kernel), the row count and the
+// row list; grown on demand, lives for the process like the library's other
+// caches
+struct SplitScratch {
+  uint32_t* hot = nullptr;
+  unsigned int* count = nullptr;
+  uint32_t* list = nullptr;
+  int64_t rows = 0;
+};
+SplitScratch* split_scratch(int64_t nrows) {
+  static std::mutex mu;
+  static SplitScratch sc[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  SplitScratch& s = sc[dev & 63];
+  if (s.rows < nrows) {
+    if (s.hot) cudaFree(s.hot);
+    s = SplitScratch{};
+    const int64_t hw = (nrows + 31) / 32 + 4;  // + the count word, 16-B aligned list
+    void* p = nullptr;
+    if (cudaMalloc(&p, (hw + nrows) * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, hw * sizeof(uint32_t)) != cudaSuccess) {
+      cudaFree(p);
+      return nullptr;
+    }
+    s.hot = static_cast<uint32_t*>(p);
+    s.count = reinterpret_cast<unsigned int*>(s.hot + (nrows + 31) / 32);
+    s.list = s.hot + hw;
+    s.rows = nrows;
+  }
+  return &s;
 }
 }  // namespace
 
@@ -728,7 +869,7 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
     const int zchunk = ZCHUNK;
     dim3 grid((unsigned)((a->nx + TX - 1) / TX), (unsigned)((a->ny + TYT - 1) / TYT),
               (unsigned)((nzu + zchunk - 1) / zchunk));
-    if (!use_tma() || !launch_built<false>(src_d, dst_d, *a, c, ti64_fields{}, nullptr,
+    if (!use_tma() || !launch_built<0>(src_d, dst_d, *a, c, ti64_fields{}, nullptr,
                                            CoupledODE{}, nzu, zchunk, st))
       built_pipe_kernel<false><<<grid, dim3(TX, TY), 0, st>>>(src_d, dst_d, *a, c, zchunk,
                                                             ti64_fields{}, nullptr, CoupledODE{});
@@ -791,10 +932,39 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   o.dt = a->dt;
   o.L = (int)lanes;
   o.rest_ok = kp->t_as_end <= kp->t_sol && kp->t_as_end <= kp->t_as_start && cfg->stuck_tol < 0.5;
+  o.hot = nullptr;
   const int zchunk = ZCHUNK;
+  if (use_tma() && coupled_split() && o.rest_ok) {  // (no cold rest: every row runs, fused)
+    const int64_t nrows = n / 32;
+    SplitScratch* sc = split_scratch(nrows);
+    if (!sc) {
+      ti64_set_error("ti64_coupled_step: split-step scratch allocation failed");
+      return TI64_ECUDA;
+    }
+    o.hot = sc->hot;
+    if (launch_built<2>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, a->z_top, zchunk, st)) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaMemsetAsync(sc->count, 0, sizeof(unsigned int), st);
+      const int64_t thr = (nrows + 3) / 4;
+      rows_scan_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(idle_bits_d, sc->hot, nrows,
+                                                                      sc->list, sc->count);
+      rows_kinetics_kernel<<<(unsigned)(sms * 8), 128, 0, st>>>(tn_d, tn1_d, *f, idle_bits_d, o,
+                                                                sc->list, sc->count);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        ti64_set_error(std::string("ti64_coupled_step: ") + cudaGetErrorString(e));
+        return TI64_ECUDA;
+      }
+      ti64_set_error("");
+      return TI64_OK;
+    }
+    o.hot = nullptr;  // grid TMA cannot map: the fused cp.async kernel below
+  }
   dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TYT - 1) / TYT),
             (unsigned)((a->z_top + zchunk - 1) / zchunk));
-  if (!use_tma() || !launch_built<true>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, a->z_top, zchunk,
+  if (!use_tma() || !launch_built<1>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, a->z_top, zchunk,
                                         st))
     built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
                                                           idle_bits_d, o);
