@@ -325,9 +325,11 @@ def measure_extra(torch, pkg, dev):
         dom.run(10, 1e-6, beams[k[0]:], src, fused=True)
         k[0] += 10
     t = _time_dev(torch, coupled, 5) / 10
-    out["config3_fused_coupled_step"] = {"cells": n, "ms_per_step": t * 1e3,
-                                        "cell_steps_per_s": n / t,
-                                        "job_estimate_s": 20000 * t}
+    out["config3_coupled_step"] = {"cells": n, "ms_per_step": t * 1e3,
+                                   "cell_steps_per_s": n / t,
+                                   "job_estimate_s": 20000 * t,
+                                   "path": "split: K4 + hot-row bitmap, row scan, kinetics of "
+                                           "listed rows (early in the job: few transformed rows)"}
     del dom
     # config 0 at its full size (4096 points x 20 000 steps, one launch)
     src0 = pkg.source_for_config(0)

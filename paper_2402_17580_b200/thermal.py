@@ -275,8 +275,10 @@ class CoupledDomain:
             thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8, fused=None):
         """n_steps coupled steps; beams[k] = (x, y, power, on) of step k.
 
-        fused=True (default when nx % 32 == 0 and no losses) runs the single-pass
-        K4+kinetics kernel with ping-pong temperatures (bit-identical results);
+        fused=True (default when nx % 32 == 0 and no losses) runs the device
+        coupled step with ping-pong temperatures (bit-identical results): the
+        stencil marking hot rows, then the kinetics of hot and transformed rows
+        only (TI64_COUPLED_FUSED=1: one K4+kinetics kernel);
         fused=False issues step_thermal + step_all per step like the reference."""
         from .batch import step_all
         from .integrator import IntegratorConfig

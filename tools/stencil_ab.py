@@ -1,5 +1,6 @@
 """Helper for tests/test_gpu_stencil.py: run K4 and the fused coupled step on
-an odd-sized grid and save the results (the pipeline is chosen by TI64_NO_TMA)."""
+an odd-sized grid and save the results (the pipeline is chosen by TI64_NO_TMA,
+the coupled-step mode by TI64_COUPLED_FUSED)."""
 import sys
 from pathlib import Path
 
@@ -21,4 +22,5 @@ for k in range(5):
                     bottom_dirichlet=353.0, all_built=True)
     b.field.temperature_old.copy_(b.field.temperature_new)
 h1 = a.fields.to_host()
-np.savez(sys.argv[1], stencil=b.field.temperature_new.cpu().numpy(), **h1)
+np.savez(sys.argv[1], stencil=b.field.temperature_new.cpu().numpy(),
+         coupled_T=a.field.temperature_old.cpu().numpy(), **h1)
