@@ -236,6 +236,9 @@ static __device__ __noinline__ void cells_step(const ti64_fields& f, uint32_t* _
   if (lane == 0 && nb != bits) idle[(flat - lane) >> 5] = nb;
 }
 
+#ifndef SPLIT_HOT_TEST
+#define SPLIT_HOT_TEST 1
+#endif
 // CM: 1 = fused (the kinetics of the warp's cells run here), 2 = split (the
 // stencil only marks rows with a hot cell; rows_kinetics_kernel runs next)
 template <int CM>
@@ -245,15 +248,22 @@ __device__ __forceinline__ void cell_kinetics(const ti64_fields& f, uint32_t* __
                                               double t_new, unsigned gm) {
   if constexpr (CM == 2) {
     // not provably cold (NaN included): the row's kinetics must run
-    // Integer screen on the high words (ALU pipe; the stencil's FP64 pipe is
-    // the busy one): |T| < t_as_end whenever hi(|T|) < hi(t_as_end), so a
-    // cell that is not flagged has T_n, T_n+1 < t_as_end; cells just below
-    // the bound and NaNs of either sign are flagged, and the kinetics kernel
-    // applies the exact test.  No vote: hot cells are rare and a warp's
-    // same-word atomics combine.
-    const int thi = __double2hiint(o.kp.t_as_end);
-    const int h = max(__double2hiint(t0) & 0x7fffffff, __double2hiint(t_new) & 0x7fffffff);
-    if (in && h >= thi) {
+    // Integer screen on the high words (ALU pipe; the stencil's FP64 pipe and
+    // issue slots are the busy ones): for T >= +0, T < t_as_end whenever
+    // hi(T) < hi(t_as_end) as unsigned, and negative values and NaNs of
+    // either sign have hi >= 0x80000000 or > hi(t_as_end) and are flagged.  So
+    // a cell that is not flagged has T_n, T_n+1 < t_as_end; cells just below
+    // the bound are flagged too, and the kinetics kernel applies the exact
+    // test.  No vote: hot cells are rare and a warp's same-word atomics
+    // combine.  (The screen costs ~20 us of the 229 us step, A/B
+    // tools/ab_split_k4.sh: no screen 208 us, masked signed compare 234 us.)
+#if SPLIT_HOT_TEST
+    const unsigned thi = (unsigned)__double2hiint(o.kp.t_as_end);
+    const unsigned h = max((unsigned)__double2hiint(t0), (unsigned)__double2hiint(t_new));
+    if (h >= thi) {
+#else  // timing experiments only: no marking (wrong results)
+    if (false) {
+#endif
       const int64_t row = flat >> 5;
       atomicOr(o.hot + (row >> 5), 1u << (row & 31));
     }
