@@ -643,6 +643,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
       // interior plane of an interior tile: all six faces present, no source
       // or boundary value; same face order and association as below
       double* dz = dcol + (int64_t)z * plane;
+      unsigned hr[RY];  // CM 2: per-row screen word, one branch per plane below
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
         const double* P = ring + s0 * SLOTD + cidx[r];
@@ -655,9 +656,25 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
         flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sp1 * SLOTD + cidx[r]], t0)));
         const double t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
         dz[(int64_t)yr[r] * nx] = t_new;
-        if (COUPLED)
+        if constexpr (CM == 2)
+          hr[r] = max((unsigned)__double2hiint(t0), (unsigned)__double2hiint(t_new));
+        else if (COUPLED)
           cell_kinetics<CM>(f, idle, o, lane, true, (int64_t)z * plane + (int64_t)yr[r] * nx + x,
                                  CM == 1 ? iring[s0 * TYT + ty + r * TY] : 0u, t0, t_new, gm);
+      }
+      if constexpr (CM == 2) {  // the screen of cell_kinetics<2>, both rows at once
+        unsigned hm = hr[0];
+#pragma unroll
+        for (int r = 1; r < RY; ++r) hm = max(hm, hr[r]);
+        const unsigned thi = (unsigned)__double2hiint(o.kp.t_as_end);
+        if (SPLIT_HOT_TEST && hm >= thi) {
+#pragma unroll
+          for (int r = 0; r < RY; ++r)
+            if (hr[r] >= thi) {
+              const int64_t row = ((int64_t)z * plane + (int64_t)yr[r] * nx + x) >> 5;
+              atomicOr(o.hot + (row >> 5), 1u << (row & 31));
+            }
+        }
       }
       __syncthreads();
       const int t = sm;
