@@ -69,6 +69,8 @@ def lib():
         L.oracle_advance.argtypes = [P, I64, P, I64, I64, I64, I64, I64, P, P,
                                      P, P, P, P, I32]
         L.oracle_advance.restype = I64
+        L.oracle_advance_points.argtypes = [P, P, I64, P, I64, I64, I64, P, P, P, P, P, I32]
+        L.oracle_advance_points.restype = I64
         L.oracle_history.argtypes = [P, P, I64, D, D, D, P, P, P]
         L.oracle_history.restype = I64
         L.oracle_stencil_step.argtypes = [P, P, P, P, P, P]
@@ -222,6 +224,46 @@ def advance(fields, gen, step0, nsteps, kp, cfg, lanes=8, snapshot_every=0,
     if rc != 0:
         raise RuntimeError(f"oracle_advance rc={rc}")
     return {"martensite": mart, "switches": sw, "totals": totals, "sums": sums}
+
+
+def advance_points(fields, points, gen, step0, nsteps, kp, cfg, threads=None, nsub=None):
+    """oracle_advance for a subset of points given by GLOBAL index (`points`,
+    int64): each point alone (width-1 lane batch), OpenMP over points.
+    `fields` (HostFields of len(points)) is advanced in place; returns
+    dict(martensite, switches, totals)."""
+    pts = np.ascontiguousarray(points, dtype=np.int64)
+    m = len(pts)
+    assert fields.n_points == m
+    nsub = num_substeps(gen.dt, cfg.dt_sub_max) if nsub is None else nsub
+    threads = max_threads() if threads is None else threads
+    mart = np.zeros(m, np.uint32)
+    sw = np.zeros(m, np.uint32)
+    totals = np.zeros(8, np.uint64)
+    fs = fields.cstruct()
+    k, c = _abi.kparams_from(kp), _abi.icfg_from(cfg)
+    rc = int(lib().oracle_advance_points(C.byref(fs), _p(pts), m, C.byref(gen), int(step0),
+                                         int(nsteps), int(nsub), C.byref(k), C.byref(c),
+                                         _p(mart), _p(sw), _p(totals), int(threads)))
+    if rc != 0:
+        raise RuntimeError(f"oracle_advance_points rc={rc}")
+    return {"martensite": mart, "switches": sw, "totals": totals}
+
+
+def gen_initial_points(gen, points):
+    """HostFields with the seeded initial state of the given GLOBAL points and
+    T_old = T(0) (as init_from_source does for a contiguous shard)."""
+    pts = np.ascontiguousarray(points, dtype=np.int64)
+    f = HostFields.allocate(len(pts))
+    g0 = _abi.TempGen.from_buffer_copy(gen)
+    for j, p in enumerate(pts):  # point_offset = p, one point at a time
+        g0.point_offset = int(p)
+        one = HostFields.allocate(1)
+        lib().oracle_gen_initial_state(C.byref(g0), 1, C.byref(one.cstruct()))
+        for k in HostFields.NAMES:
+            getattr(f, k)[j] = getattr(one, k)[0]
+        f.temperature_old[j] = lib().oracle_gen_temperature1(C.byref(g0), 0, 0)
+    f.temperature_new[:] = f.temperature_old
+    return f
 
 
 def history(times, temps, state0, kp, cfg):

@@ -638,57 +638,91 @@ static inline double pulse(double a, double tc, double inv_w, double t) {
   return a * oracle_fast_exp1(-(u * u));
 }
 
-double oracle_gen_temperature1(const ti64_tempgen* g, int64_t local, int64_t step) {
-  const uint64_t pt = (uint64_t)(g->point_offset + local);
-  const double t = (double)step * g->dt;
+/* One point's generator with its seeded parameters drawn once (the per-step
+ * arithmetic is the definition; drawing once only saves the hashes). */
+#define PG_MAXP 64
+typedef struct {
+  int np;
+  double a[PG_MAXP], tc[PG_MAXP], inv_w[PG_MAXP];
+  double x, y, dd;
+} pointgen;
+
+static void pointgen_init(const ti64_tempgen* g, uint64_t pt, pointgen* q) {
   const double* p = g->p;
+  q->np = 0;
   switch (g->kind) {
     case TI64_SRC_PULSE: {
       double a = unif(p[0], p[1], u01(g->seed, pt, 0));
       double tc = unif(p[2], p[3], u01(g->seed, pt, 1));
       double w = unif(p[4], p[5], u01(g->seed, pt, 2));
-      double inv_w = 1.0 / w;
-      return g->base + pulse(a, tc, inv_w, t);
+      q->np = 1;
+      q->a[0] = a;
+      q->tc[0] = tc;
+      q->inv_w[0] = 1.0 / w;
+      break;
     }
     case TI64_SRC_ROSENTHAL: {
       int64_t i = (int64_t)pt % g->nx;
       int64_t j = ((int64_t)pt / g->nx) % g->ny;
       int64_t k = (int64_t)pt / (g->nx * g->ny);
-      double x = (double)i * g->h, y = (double)j * g->h, d = (double)k * g->h;
-      const double* b = g->beam_d + 3 * step;
-      double xi = (x - b[0]) * b[2];
-      double eta = y - b[1];
-      double r = sqrt(xi * xi + eta * eta + d * d);
-      double tt = g->base + p[0] / r * oracle_fast_exp1(-(p[1] * (r + xi)));
-      return tt > p[2] ? p[2] : tt;
+      double d = (double)k * g->h;
+      q->x = (double)i * g->h;
+      q->y = (double)j * g->h;
+      q->dd = d * d;
+      break;
     }
     case TI64_SRC_PULSE_TRAIN: {
       double a1 = unif(p[0], p[1], u01(g->seed, pt, 0));
-      double s = g->base;
       double scale = 1.0;
-      for (int kk = 0; kk < g->max_pulses; ++kk) {
-        double a = a1 * scale * unif(p[2], p[3], u01(g->seed, pt, 1 + 3 * kk));
-        double tc = p[4] + p[5] * (double)kk + unif(p[6], p[7], u01(g->seed, pt, 2 + 3 * kk));
-        double w = unif(p[8], p[9], u01(g->seed, pt, 3 + 3 * kk));
-        s = s + pulse(a, tc, 1.0 / w, t);
+      int np_ = g->max_pulses < PG_MAXP ? g->max_pulses : PG_MAXP;
+      for (int kk = 0; kk < np_; ++kk) {
+        q->a[kk] = a1 * scale * unif(p[2], p[3], u01(g->seed, pt, 1 + 3 * kk));
+        q->tc[kk] = p[4] + p[5] * (double)kk + unif(p[6], p[7], u01(g->seed, pt, 2 + 3 * kk));
+        q->inv_w[kk] = 1.0 / unif(p[8], p[9], u01(g->seed, pt, 3 + 3 * kk));
         scale = scale * p[10];
       }
-      return s;
+      q->np = np_;
+      break;
     }
     case TI64_SRC_PULSE_SWEEP: {
       int np_ = 1 + (int)(u01(g->seed, pt, 0) * (double)g->max_pulses);
-      double s = g->base;
+      if (np_ > PG_MAXP) np_ = PG_MAXP;
       for (int kk = 0; kk < np_; ++kk) {
-        double a = unif(p[0], p[1], u01(g->seed, pt, 1 + 3 * kk));
-        double tc = unif(p[2], p[3], u01(g->seed, pt, 2 + 3 * kk));
-        double w = oracle_fast_exp1(unif(p[4], p[5], u01(g->seed, pt, 3 + 3 * kk)));
-        s = s + pulse(a, tc, 1.0 / w, t);
+        q->a[kk] = unif(p[0], p[1], u01(g->seed, pt, 1 + 3 * kk));
+        q->tc[kk] = unif(p[2], p[3], u01(g->seed, pt, 2 + 3 * kk));
+        q->inv_w[kk] = 1.0 / oracle_fast_exp1(unif(p[4], p[5], u01(g->seed, pt, 3 + 3 * kk)));
       }
-      return s;
+      q->np = np_;
+      break;
     }
     default:
-      return qnan();
+      break;
   }
+}
+
+/* T at time step `step` (t = step * dt): base + the pulses in order k = 1..K,
+ * or the capped Rosenthal term */
+static double pointgen_temp(const ti64_tempgen* g, const pointgen* q, int64_t step) {
+  const double t = (double)step * g->dt;
+  const double* p = g->p;
+  if (g->kind == TI64_SRC_ROSENTHAL) {
+    const double* b = g->beam_d + 3 * step;
+    double xi = (q->x - b[0]) * b[2];
+    double eta = q->y - b[1];
+    double r = sqrt(xi * xi + eta * eta + q->dd);
+    double tt = g->base + p[0] / r * oracle_fast_exp1(-(p[1] * (r + xi)));
+    return tt > p[2] ? p[2] : tt;
+  }
+  if (g->kind < TI64_SRC_PULSE || g->kind > TI64_SRC_PULSE_SWEEP) return qnan();
+  double s = g->base;
+  for (int kk = 0; kk < q->np; ++kk) s = s + pulse(q->a[kk], q->tc[kk], q->inv_w[kk], t);
+  return s;
+}
+
+double oracle_gen_temperature1(const ti64_tempgen* g, int64_t local, int64_t step) {
+  pointgen q;
+  pointgen_init(g, (uint64_t)(g->point_offset + local), &q);
+  return pointgen_temp(g, &q, step);
 }
 
 void oracle_gen_temperature(const ti64_tempgen* g, int64_t n, int64_t step, double* out,
@@ -803,6 +837,74 @@ int64_t oracle_advance(const ti64_fields* f, int64_t n, const ti64_tempgen* g,
   free(xm_prev);
   free(am_prev);
   return 0;
+}
+
+/* The reference loop of oracle_advance for a SUBSET of points given by their
+ * GLOBAL indices pts[0..m) (e.g. every 1024th point of a config): points are
+ * independent, so each runs alone as a width-1 lane batch (explicit-scheme
+ * states are lane-width invariant, test_batch.py:79-85; the seed arrays of
+ * inactive points are lane-width-dependent residue and are not compared).
+ * f holds the m points' state (in/out); counters as oracle_advance
+ * (per-point mart/sw may be NULL; totals[8] may be NULL). */
+int64_t oracle_advance_points(const ti64_fields* f, const int64_t* pts, int64_t m,
+                              const ti64_tempgen* g, int64_t step0, int64_t nsteps,
+                              int64_t nsub, const ti64_kparams* kp, const ti64_icfg* cfg,
+                              uint32_t* mart, uint32_t* sw, uint64_t* totals,
+                              int32_t threads) {
+  int64_t rc_all = 0;
+  uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, t6 = 0, t7 = 0;
+  const double dt_sub = g->dt / (double)nsub;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 16) num_threads(threads > 0 ? threads : 1) \
+    reduction(max : rc_all) reduction(+ : t0, t1, t2, t3, t4, t5, t6, t7)
+#endif
+  for (int64_t j = 0; j < m; ++j) {
+    pointgen q;
+    pointgen_init(g, (uint64_t)pts[j], &q);
+    ti64_fields fj = {f->x_alpha_s + j,    f->x_alpha_m + j,    f->x_beta + j,
+                      f->temperature_old + j, f->temperature_new + j, f->seed_tracked + j,
+                      f->seed_active + j,  f->seed_direction + j};
+    uint32_t mc = 0, sc = 0;
+    for (int64_t s = 0; s < nsteps; ++s) {
+      const double T1 = pointgen_temp(g, &q, step0 + s + 1);
+      f->temperature_new[j] = T1;
+      const double xs = f->x_alpha_s[j], xm = f->x_alpha_m[j];
+      const double xa = xs + xm;
+      const double xe0 = xaeq_of(f->temperature_old[j], kp);
+      const int grow = (xa < xe0) & (xs > 0.0);
+      const int am = (xm > 0.0) & (xs > 0.0);
+      const int dis = (xa > xe0) & (xa < XA_MAX);
+      t1 += T1 < kp->t_am_start;
+      t2 += grow | am;
+      t3 += grow;
+      t4 += am;
+      t5 += dis;
+      const int amx = argmax3(xs, xm, f->x_beta[j]);
+      int64_t rc = oracle_run_range(&fj, 0, 1, 1, nsub, dt_sub, kp, cfg);
+      if (rc != 0) {
+        if (rc_all < j + 1) rc_all = j + 1;
+        break;
+      }
+      mc += f->x_alpha_m[j] > xm;
+      sc += argmax3(f->x_alpha_s[j], f->x_alpha_m[j], f->x_beta[j]) != amx;
+    }
+    if (mart) mart[j] += mc;
+    if (sw) sw[j] += sc;
+    t0 += (uint64_t)nsteps;
+    t6 += mc;
+    t7 += sc;
+  }
+  if (totals) {
+    totals[0] += t0;
+    totals[1] += t1;
+    totals[2] += t2;
+    totals[3] += t3;
+    totals[4] += t4;
+    totals[5] += t5;
+    totals[6] += t6;
+    totals[7] += t7;
+  }
+  return rc_all;
 }
 
 /* integrator.py:328-361 _history_kernel for one point (times strictly

@@ -10,11 +10,9 @@ from pathlib import Path
 
 from . import _abi
 
-import os
-
-# TI64_LIB overrides the in-tree library (kernel-variant experiments only)
-LIB_PATH = Path(os.environ.get("TI64_LIB") or
-                Path(__file__).resolve().parent / "_lib" / "libti64b200.so")
+# The in-tree library; there is no environment override (kernel-variant A/B
+# experiments live in tools/ and patch LIB_PATH explicitly, tools/_variant.py).
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libti64b200.so"
 
 __all__ = ["Ti64Unavailable", "Ti64Error", "load", "require", "check", "LIB_PATH"]
 

@@ -189,6 +189,21 @@ def branch_dispatch(mask):
     return "some"
 
 
+def _keep_for_stream(stream, *tensors):
+    """Temporaries allocated on the current stream but used by kernels queued
+    on a caller-supplied `stream`: tell torch's caching allocator, so their
+    memory is not handed out again before that stream's queued work is done
+    (record_stream)."""
+    if stream is None:
+        return
+    torch = _torch()
+    if stream == torch.cuda.current_stream():
+        return
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
+
+
 def _kp(params):
     return _abi.kparams_from(params.kernel_tuple())
 
@@ -247,6 +262,7 @@ def step_all(fields, dt, params=DEFAULT_PARAMS, config=IntegratorConfig(), n_lan
         iters = _torch().zeros(n, dtype=_torch().int64, device=fields.compute_device)
     rc = run_range(fields, 0, n, n_lanes, nsub, float(dt) / nsub, params.kernel_tuple(),
                    config.kernel_tuple(), record_iters, iters, stream)
+    _keep_for_stream(stream, iters)
     fields.traffic_bytes += BYTES_PER_POINT * n
     fields.steps_taken += 1
     if rc > 0:
@@ -286,19 +302,24 @@ class AdvanceResult:
     launches: int
 
 
-_beam_cache = {}
+_beam_cache = {}  # insertion-ordered: LRU eviction of the oldest entry
+_BEAM_CACHE_MAX = 8
 
 
 def beam_table(source, rows, device):
+    """Device beam table of `source` (None for pulse sources), cached.  An
+    evicted table is only released through torch's caching allocator, which
+    is stream-ordered; callers launching on another stream record it there
+    (_keep_for_stream), so a queued kernel never reads reused memory."""
     key = (source, rows, str(device))
-    t = _beam_cache.get(key)
+    t = _beam_cache.pop(key, None) if key in _beam_cache else None
     if t is None:
         packed = getattr(source, "packed_beam", None)
         tab = packed(rows) if packed is not None else source.beam_table(rows)
         t = None if tab is None else _torch().from_numpy(tab).to(device)
-        if len(_beam_cache) > 8:
-            _beam_cache.clear()
-        _beam_cache[key] = t
+        while len(_beam_cache) >= _BEAM_CACHE_MAX:
+            _beam_cache.pop(next(iter(_beam_cache)))
+    _beam_cache[key] = t
     return t
 
 
@@ -355,7 +376,8 @@ def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
                           None if cs is None else C.byref(cs), _lib.ptr(sums),
                           _lib.ptr(scratch), _lib.stream_handle(stream))
     launches = _lib.check(rc, "ti64_advance")  # >= 0: kernels launched
-    del beam  # kernels are queued; the cache keeps the table alive
+    _keep_for_stream(stream, beam, sums, scratch)
+    del beam
     fields.traffic_bytes += BYTES_PER_POINT * n * n_steps
     fields.steps_taken += n_steps
     return AdvanceResult(sums=sums[:n_snap], counters=counters, steps=n_steps,
@@ -411,6 +433,7 @@ def _advance_implicit(fields, n_steps, source, step0, params, config, n_lanes,
                                            n, _lib.ptr(sums[snap]), _lib.ptr(scratch),
                                            _lib.stream_handle(stream)), "ti64_phase_sums")
             launches += 2
+    _keep_for_stream(stream, beam, sums, scratch)
     del beam
     return AdvanceResult(sums=sums, counters=None, steps=n_steps, launches=launches)
 

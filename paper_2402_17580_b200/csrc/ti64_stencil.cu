@@ -236,9 +236,6 @@ static __device__ __noinline__ void cells_step(const ti64_fields& f, uint32_t* _
   if (lane == 0 && nb != bits) idle[(flat - lane) >> 5] = nb;
 }
 
-#ifndef SPLIT_HOT_TEST
-#define SPLIT_HOT_TEST 1
-#endif
 // CM: 1 = fused (the kinetics of the warp's cells run here), 2 = split (the
 // stencil only marks rows with a hot cell; rows_kinetics_kernel runs next)
 template <int CM>
@@ -257,13 +254,9 @@ __device__ __forceinline__ void cell_kinetics(const ti64_fields& f, uint32_t* __
     // test.  No vote: hot cells are rare and a warp's same-word atomics
     // combine.  (The screen costs ~20 us of the 229 us step, A/B
     // tools/ab_split_k4.sh: no screen 208 us, masked signed compare 234 us.)
-#if SPLIT_HOT_TEST
     const unsigned thi = (unsigned)__double2hiint(o.kp.t_as_end);
     const unsigned h = max((unsigned)__double2hiint(t0), (unsigned)__double2hiint(t_new));
     if (h >= thi) {
-#else  // timing experiments only: no marking (wrong results)
-    if (false) {
-#endif
       const int64_t row = flat >> 5;
       atomicOr(o.hot + (row >> 5), 1u << (row & 31));
     }
@@ -667,7 +660,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
 #pragma unroll
         for (int r = 1; r < RY; ++r) hm = max(hm, hr[r]);
         const unsigned thi = (unsigned)__double2hiint(o.kp.t_as_end);
-        if (SPLIT_HOT_TEST && hm >= thi) {
+        if (hm >= thi) {
 #pragma unroll
           for (int r = 0; r < RY; ++r)
             if (hr[r] >= thi) {
@@ -684,9 +677,6 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
       si = t;
       continue;
     }
-    double tm_[RY];
-#pragma unroll
-    for (int r = 0; r < RY; ++r) tm_[r] = 0.0;
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
       if (yr[r] < ny) {  // warp-uniform (one warp per x-row)
@@ -713,7 +703,6 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
                                  CM == 1 ? iring[s0 * TYT + ty + r * TY] : 0u, t0, t_new, gm);
       }
     }
-    (void)tm_;
     __syncthreads();  // every thread is done with slot sm before it is refilled
     const int t = sm;
     sm = s0;

@@ -5,8 +5,9 @@
 # plus the config-1 job (bench --quick).  Usage: tools/ab_active.sh A B ...
 for rep in 1 2; do
   for v in "$@"; do
-    TI64_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python - <<PY
+    TI64_VARIANT_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python - <<PY
 import json, subprocess, sys, torch
+import sys; sys.path.insert(0, "tools"); import _variant  # noqa
 import paper_2402_17580_b200 as pkg
 from paper_2402_17580_b200.batch import gen_temperature
 dev = torch.device("cuda", 0)
@@ -35,5 +36,5 @@ done
 # single-task step latency of config 1 (the 32 surface points 0..31 alone)
 for v in "$@"; do
   echo -n "$v cfg1 single task: "
-  TI64_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python tools/prof_advance.py --config 1 --n 32 --steps 10000 --reps 3 | tail -1
+  TI64_VARIANT_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python tools/prof_advance.py --config 1 --n 32 --steps 10000 --reps 3 | tail -1
 done

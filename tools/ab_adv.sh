@@ -3,8 +3,9 @@
 # (bench --quick) and the config 2/4 2^22-point shards
 for rep in 1 2; do
   for v in "$@"; do
-    TI64_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python - <<PY
+    TI64_VARIANT_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python - <<PY
 import json, subprocess, sys, torch
+import sys; sys.path.insert(0, "tools"); import _variant  # noqa
 import paper_2402_17580_b200 as pkg
 dev = torch.device("cuda", 0)
 out = []

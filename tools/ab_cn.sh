@@ -2,8 +2,9 @@
 # interleaved A/B of the implicit step_all (block-100 layout, 2^22 points)
 for rep in 1 2; do
   for v in "$@"; do
-    TI64_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python - <<PY
+    TI64_VARIANT_LIB=paper_2402_17580_b200/_lib/variants/lib_$v.so python - <<PY
 import torch, bench
+import sys; sys.path.insert(0, "tools"); import _variant  # noqa
 import paper_2402_17580_b200 as pkg
 dev = torch.device("cuda", 0)
 cfg = pkg.IntegratorConfig(scheme="crank_nicolson", dt_sub_max=0.01)

@@ -11,6 +11,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 import torch  # noqa: E402
 
+import _variant  # noqa: E402,F401  (tools only: optional TI64_VARIANT_LIB)
 import paper_2402_17580_b200 as pkg  # noqa: E402
 
 ap = argparse.ArgumentParser()

@@ -2,13 +2,14 @@
     python tools/build_variant.py NAME [--rev GITREV] [-DFOO=1 ...]
         -> paper_2402_17580_b200/_lib/variants/lib_NAME.so
 --rev builds the sources (csrc + include) of that git revision instead of the
-working tree.  Select a variant at run time with TI64_LIB=<path>."""
+working tree.  Select a variant at run time with TI64_VARIANT_LIB=<path>."""
 import subprocess
 import sys
 import tempfile
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import _variant  # noqa: E402,F401  (tools only: optional TI64_VARIANT_LIB)
 from paper_2402_17580_b200 import _build as b  # noqa: E402
 
 args = sys.argv[1:]

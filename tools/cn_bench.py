@@ -11,6 +11,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+import _variant  # noqa: E402,F401  (tools only: optional TI64_VARIANT_LIB)
 import paper_2402_17580_b200 as pkg  # noqa: E402
 from paper_2402_17580_b200 import _lib  # noqa: E402
 

@@ -3,6 +3,7 @@ from the same start, every state array compared bit for bit."""
 import sys
 sys.path.insert(0, '.')
 import numpy as np, torch
+import _variant  # noqa: E402,F401  (tools only: optional TI64_VARIANT_LIB)
 import paper_2402_17580_b200 as pkg
 from paper_2402_17580_b200 import scanpath, thermal as th
 dev = torch.device("cuda", 0)

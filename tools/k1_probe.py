@@ -4,6 +4,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
+import _variant  # noqa: E402,F401  (tools only: optional TI64_VARIANT_LIB)
 import paper_2402_17580_b200 as pkg  # noqa: E402
 
 n = 1 << 26

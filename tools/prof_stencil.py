@@ -3,6 +3,7 @@ import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
+import _variant  # noqa: E402,F401  (tools only: optional TI64_VARIANT_LIB)
 from paper_2402_17580_b200 import thermal as th, scanpath  # noqa: E402
 
 nz, ny, nx = 256, 512, 512

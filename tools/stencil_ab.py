@@ -7,6 +7,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
 
+import _variant  # noqa: E402,F401  (tools only: optional TI64_VARIANT_LIB)
 from paper_2402_17580_b200 import scanpath, thermal as th  # noqa: E402
 
 nz, ny, nx, h, dt = 21, 37, 64, 20e-6, 1e-6
