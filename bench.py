@@ -1,25 +1,39 @@
 #!/usr/bin/env python
 """bench.py — microstructure point-updates/s (fp64) on B200.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-N = 2^20 points on a 128x128x64 lattice, 10,000 explicit steps of dt = 2e-5 s,
-temperatures from the on-device Rosenthal raster generator,
-initial state (0.9, 0, 0.1).  One bench "step" = that whole job: 10,000
-time steps over all 2^20 points (1.05e10 point-updates), run by ONE launch
-of the fused advance kernel (K2) that records the phase sums after every
-1,000 steps (per-task sums reduced by one small kernel at the end).
-Weak scaling: each rank runs its own copy of the job (one GPU per rank).
+Headline workload: BASELINE.json configs[4], the largest configuration that
+fits one GPU (the metric string names no config, so the largest one is the
+one it is quoted on): N = 2^27 points, per-point seeded histories of 1-20
+Gaussian pulses (peaks U(600, 3000) K, widths log-uniform on [1e-4, 1e-2] s,
+centres U(0, 1) s, base 300 K), dt = 1e-5 s, a 100 000-step job; every point
+is advanced by the explicit update each step.
+
+One bench "step" = one WINDOW of 200 consecutive time steps of that job over
+all 2^27 points (5.4e9 point-updates), run by one launch of the fused
+advance kernel K2 (+ the snapshot phase-sum kernel).  The state is prepared
+untimed up to step 20 000 (where the per-window rate has reached the
+whole-job average to within a few %, tools/window_rates.py), then W warm-up
+windows, then K timed windows: steps 20 000 + 200 W ... of the real job.
+The timed region ends with the 3x256-bin phase-fraction histogram and the
+cross-rank all-reduce of sums, histogram and counters.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-`--impl reference` times the reference's CPU algorithm (the C oracle port,
-oracle/ti64_oracle.c, OpenMP over all host cores) on the same workload and
-prints the same JSON line with "impl": "reference".
+--gpus N without torchrun spawns N ranks itself (one process per GPU,
+127.0.0.1 rendezvous); the 2^27 points are sharded in contiguous blocks
+(strong scaling: total work fixed); max-over-ranks device time.
+
+--impl reference times the reference's own CPU implementation (ti64micro's
+numba step_all from baseline/_ref, n_lanes=8, all host threads) on a bounded
+sample of the same windows: every 1024th point of the 2^27, state prepared
+by the oracle (bit-identical to the reference, checked on the sample), the
+per-step temperatures generated outside the timed region.
 """
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,21 +48,34 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "microstructure point-updates/s (fp64)"
 UNIT = "point-updates/s"
-JOB_STEPS = 10_000
-SNAP_EVERY = int(os.environ.get("TI64_BENCH_SNAP", "1000"))  # snapshot interval (steps)
-# DRAM bytes (read + write) of the job's single K2 launch, from the committed
-# ncu capture profiles/r01b_advance_cfg1_job.txt (44.59 MB + 7.66 MB)
-K2_JOB_DRAM_BYTES = 44_589_568 + 7_659_776
-# executed view of the same launch (same capture): FP64 pipe and issue activity
-K2_JOB_EXECUTED = {"fp64_pipe_active": 0.2742, "issue_active": 0.4936, "warps_active": 0.1599,
-                   "source": "profiles/r01b_advance_cfg1_job.txt (ncu --set full: "
-                             "sm__pipe_fp64_cycles_active, smsp__issue_active, sm__warps_active)"}
-WORKLOAD = ("config1: Rosenthal raster (200 W, eta 0.35, 1 m/s, 100 um hatch), "
-            "N=2^20 points on 128x128x64 lattice h=20um, 10000 steps dt=2e-5 s, "
-            "state (0.9,0,0.1)")
-# Algorithmic flops per point-update (bench.py:45-58 counts):
+HEADLINE = 4
+# per config: total points, job steps, window steps (one bench step), start
+# step of the warm-up windows, stride of the CPU sample (global indices)
+CONFIGS = {
+    4: dict(n=1 << 27, job=100_000, window=200, start=20_000, stride=1024),
+    2: dict(n=1 << 24, job=50_000, window=200, start=10_000, stride=128),
+    1: dict(n=1 << 20, job=10_000, window=10_000, start=0, stride=8),
+    0: dict(n=4096, job=20_000, window=20_000, start=0, stride=1),
+}
+WORKLOADS = {
+    4: "config4: 1-20 Gaussian pulses/point, peaks U(600,3000) K, widths log-U[1e-4,1e-2] s, "
+       "centres U(0,1) s, base 300 K; N=2^27 points, dt=1e-5 s, 100000-step job",
+    2: "config2: 10 re-scan pulses on 353 K, seeded xs0 U(0.8,0.95); N=2^24, dt=1e-5 s, "
+       "50000-step job",
+    1: "config1: Rosenthal raster (200 W, eta 0.35, 1 m/s, 100 um hatch) on a 128x128x64 "
+       "lattice h=20um; N=2^20, dt=2e-5 s, 10000-step job",
+    0: "config0: one Gaussian pulse/point; N=4096, dt=1e-5 s, 20000-step job",
+}
+# Algorithmic flops per point-update (the reference's count_flops
+# constants bench.py:45-58 at n_lanes=1, minus the carried T_n functions):
 # F = 48 + 22[T1<848] + 46[grow|am] + 49[grow] + 49[am] + 98[dissolve] + 18
 F_BASE, F_FORM, F_GA, F_GROW, F_AM, F_DIS, F_TAIL = 48, 22, 46, 49, 49, 98, 18
+# executed view and DRAM traffic of the headline launch, from the committed
+# ncu capture of the bench workload (profiles/README.md, round 2)
+K2_PROFILE = {
+    "file": "profiles/r02_advance_cfg4_window.txt",
+    "dram_bytes_per_launch": None, "fp64_pipe_active": None, "issue_active": None,
+}
 
 
 def log(*a):
@@ -58,6 +85,44 @@ def log(*a):
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def config_dict(cfg_id, n_gpus, K, W):
+    c = CONFIGS[cfg_id]
+    t0 = c["start"] + W * c["window"]
+    d = {"workload": WORKLOADS[cfg_id], "config_id": cfg_id, "points": c["n"],
+         "job_steps": c["job"], "window_steps": c["window"],
+         "timed_steps": [t0, t0 + K * c["window"]],
+         "step": f"{c['window']} consecutive time steps of the job over all points",
+         "l2": "inputs larger than L2 (state 50 B/point)" if c["n"] * 50 > (256 << 20)
+         else "L2 flushed between timed iterations (256 MiB write)",
+         "parallelism": f"points sharded in contiguous blocks over {n_gpus} GPU(s), "
+                        "no communication until the final all-reduce"}
+    return d
+
+
+# ---------------------------------------------------------------------------
+# launching: one process per GPU
+# ---------------------------------------------------------------------------
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n, argv):
+    """Run this script as n ranks (RANK/LOCAL_RANK/WORLD_SIZE/MASTER_*), as
+    torchrun would; rank 0's stdout is this process's stdout."""
+    port = free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *argv],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
 
 
 class ClockSampler:
@@ -156,7 +221,6 @@ def reference_flops(xs, xm, t0, t1, n_lanes, scheme="explicit", mean_iters=None,
     xa = xs + xm
     fl = 2 * R_TFUNCS * pad
     fl += R_XMEQ * n_lanes * int((t1 < p.t_alpha_m_start).any(axis=1).sum())
-    # x_alpha_eq(T_old) with numpy exp: only the branch masks depend on it
     ramp = 1.0 - np.exp(-p.k_alpha_eq * (p.t_alpha_s_start - t0))
     xaeq0 = np.where(t0 < p.t_alpha_s_end, 0.9, np.where(t0 > p.t_alpha_s_start, 0.0, ramp))
     grow = (xa < xaeq0) & (xs > 0.0)
@@ -175,10 +239,7 @@ def reference_flops(xs, xm, t0, t1, n_lanes, scheme="explicit", mean_iters=None,
 
 
 def branch_layout(block, n, seed=0):
-    """The reference's CPU-benchmark layout (bench.py:62-80 generate_layout):
-    alternating blocks of cooling mid-transformation points (beta -> alpha_s
-    growth, ~1000 K) and heating points above equilibrium (alpha_s
-    dissolution, ~1150 K).  numpy's seeded generator, as there."""
+    """The reference's CPU-benchmark layout (bench.py:62-80 generate_layout)."""
     rng = np.random.default_rng(seed)
     odd = (np.arange(n) // block) % 2 == 1
     t_old = np.where(odd, 1150.0, 1000.0) + rng.uniform(-20.0, 20.0, n)
@@ -189,61 +250,193 @@ def branch_layout(block, n, seed=0):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm / cpu_baseline: the C oracle (port of the reference
-# algorithm) on the box's host cores.
+# CPU legs (the oracle port and the reference itself) on a strided sample
 # ---------------------------------------------------------------------------
 
-def cpu_reference(budget_s=12.0, max_steps=JOB_STEPS, threads=None):
-    """Time the oracle's step_all (lanes=8, all host threads) on config 1.
-    Temperatures are generated per step outside the timed region."""
+NAMES = ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old", "temperature_new",
+         "seed_tracked", "seed_active", "seed_direction")
+
+
+def cpu_threads():
+    return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_windows(step_fn, fields, gen, pts, t0, window, max_windows, budget_s, threads):
+    """Run whole windows of step_fn(fields) from step t0 with the sample's
+    temperatures generated outside the timed region; returns (seconds,
+    windows)."""
+    from oracle import oracle as orc
+    timed, done = 0.0, 0
+    while done < max_windows and (done == 0 or timed < budget_s):
+        T = orc.gen_temperature_points(gen, pts, t0 + done * window + 1, window, threads)
+        for s in range(window):
+            fields.temperature_new[:] = T[s]
+            c0 = time.perf_counter()
+            step_fn(fields)
+            timed += time.perf_counter() - c0
+        done += 1
+    return timed, done
+
+
+def oracle_sample_rate(cfg_id, state, pts, t0, max_windows, budget_s):
+    """The oracle port's step_all (lanes=8, OpenMP over all host threads) on
+    the sample, from `state` (numpy arrays of the sample at step t0)."""
     from oracle import oracle as orc
     from paper_2402_17580_b200 import sources
-    from paper_2402_17580_b200.kinetics import DEFAULT_PARAMS
     from paper_2402_17580_b200.integrator import IntegratorConfig
-    threads = threads or os.cpu_count() or 1
-    src = sources.source_for_config(1)
-    n = src.n_points
-    tab = src.beam_table(max_steps + 1)
-    g = src.tempgen(0, tab.ctypes.data, len(tab))
-    f = orc.gen_initial_state(g, n)
-    f.temperature_old[:] = orc.gen_temperature(g, n, 0, threads)
+    from paper_2402_17580_b200.kinetics import DEFAULT_PARAMS
+    c = CONFIGS[cfg_id]
+    src = sources.source_for_config(cfg_id)
+    gen = src.tempgen(point_offset=0, **_beam_kw(src, c["job"] + 1))
+    threads = cpu_threads()
     kp = DEFAULT_PARAMS.kernel_tuple()
     cfg = IntegratorConfig().kernel_tuple()
-    # warm-up (first touch, thread pool)
-    f.temperature_new[:] = orc.gen_temperature(g, n, 1, threads)
-    w = f.copy()
-    orc.step_all(w, src.dt, kp, cfg, n_lanes=8, threads=threads)
-    timed, steps = 0.0, 0
-    while steps < max_steps and timed < budget_s:
-        f.temperature_new[:] = orc.gen_temperature(g, n, steps + 1, threads)
-        t0 = time.perf_counter()
-        orc.step_all(f, src.dt, kp, cfg, n_lanes=8, threads=threads)
-        timed += time.perf_counter() - t0
-        steps += 1
-    ups = n * steps / timed
-    return {"value": ups, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"config-1 lattice, all {n} points x first {steps} of {JOB_STEPS} "
-                      f"steps, oracle step_all (lanes=8, OpenMP {threads} threads), "
-                      f"T generated outside the timed region; {timed:.1f} s timed",
-            "seconds": timed}
+    f = orc.HostFields(*[state[k] for k in NAMES])
+    secs, wins = cpu_windows(lambda fl: orc.step_all(fl, src.dt, kp, cfg, n_lanes=8,
+                                                     threads=threads),
+                             f, gen, pts, t0, c["window"], max_windows, budget_s, threads)
+    upd = len(pts) * c["window"] * wins
+    return {"value": upd / secs, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"every {c['stride']}th point ({len(pts)} points) x {wins} window(s) of "
+                      f"{c['window']} steps from step {t0}; oracle/ti64_oracle.c step_all "
+                      f"(lanes=8, OpenMP {threads} threads on {cpu_model()}), T generated "
+                      f"outside the timed region; {secs:.1f} s timed",
+            "seconds": secs, "windows": wins, "fields": f}
+
+
+_BEAMS = {}
+
+
+def _beam_kw(src, rows):
+    """Host beam table for the oracle's Rosenthal generator (config 1)."""
+    tab_fn = getattr(src, "beam_table", None)
+    if tab_fn is None:
+        return {}
+    tab = _BEAMS.get((src, rows))
+    if tab is None:
+        tab = tab_fn(rows)
+        if tab is None:
+            return {}
+        tab = np.ascontiguousarray(tab)
+        _BEAMS[(src, rows)] = tab
+    return {"beam_ptr": tab.ctypes.data, "beam_steps": rows}
+
+
+def import_reference():
+    """ti64micro (the unmodified reference) from baseline/_ref, or None."""
+    # the unresolved /root/repo path (a symlink to the run directory on the
+    # GPU box): numba keys its on-disk cache by the source path, so a stable
+    # path lets a cache made on one box serve the next
+    stable = Path("/root/repo/baseline/_ref")
+    ref = stable if (stable / "ti64micro").exists() else ROOT / "baseline" / "_ref"
+    if not (ref / "ti64micro").exists():
+        return None, "baseline/_ref/ti64micro missing"
+    cache = ref / ".numba_cache"
+    try:
+        cache.mkdir(exist_ok=True)
+        os.environ.setdefault("NUMBA_CACHE_DIR", str(cache))
+    except OSError:
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ti64_numba_cache")
+    os.environ.setdefault("NUMBA_NUM_THREADS", str(cpu_threads()))
+    sys.path.insert(0, str(ref))
+    try:
+        import ti64micro  # noqa: F401
+        from ti64micro import batch, integrator, kinetics
+        return (batch, integrator, kinetics), None
+    except Exception as e:  # numba missing on the box, etc.
+        return None, f"{type(e).__name__}: {e}"
 
 
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    base = cpu_reference(budget_s=max(2.0, min(30.0, 1.5 * args.steps)))
-    line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * (1 << 20) * JOB_STEPS / base["value"],
-            "higher_is_better": True, "scaling": "weak",
+    cfg_id = HEADLINE
+    c = CONFIGS[cfg_id]
+    from oracle import oracle as orc
+    from paper_2402_17580_b200 import sources
+    from paper_2402_17580_b200.integrator import IntegratorConfig
+    from paper_2402_17580_b200.kinetics import DEFAULT_PARAMS
+    src = sources.source_for_config(cfg_id)
+    gen = src.tempgen(point_offset=0)
+    threads = cpu_threads()
+    pts = np.arange(0, c["n"], c["stride"], dtype=np.int64)
+    t_start = c["start"] + args.warmup * c["window"]
+    kp = DEFAULT_PARAMS.kernel_tuple()
+    icfg = IntegratorConfig().kernel_tuple()
+    # state of the sample at the first timed step: the oracle (bit-identical
+    # to the reference, checked below on the timed windows)
+    c0 = time.perf_counter()
+    h = orc.gen_initial_points(gen, pts)
+    orc.advance_points(h, pts, gen, 0, t_start, kp, icfg, threads=threads)
+    prep_s = time.perf_counter() - c0
+    start_state = {k: getattr(h, k).copy() for k in NAMES}
+    mods, why = import_reference()
+    kind, jit_s, check = "reference", None, None
+    if mods is not None:
+        rbatch, rinteg, rkin = mods
+        import numba
+        rf = rbatch.GlobalFields(*[start_state[k].copy() for k in NAMES[:5]],
+                                 seed_tracked=start_state["seed_tracked"].copy(),
+                                 seed_active=start_state["seed_active"].copy(),
+                                 seed_direction=start_state["seed_direction"].copy())
+        rcfg = rinteg.IntegratorConfig(scheme="explicit")
+        c0 = time.perf_counter()
+        warm = rbatch.GlobalFields(*[start_state[k][:64].copy() for k in NAMES[:5]])
+        rbatch.step_all(warm, src.dt, rkin.DEFAULT_PARAMS, rcfg, n_lanes=8, threads=threads)
+        jit_s = time.perf_counter() - c0
+        secs, wins = cpu_windows(
+            lambda fl: rbatch.step_all(fl, src.dt, rkin.DEFAULT_PARAMS, rcfg, n_lanes=8,
+                                       threads=threads),
+            rf, gen, pts, t_start, c["window"], args.steps, 1e30, threads)
+        layer = numba.threading_layer()
+        desc = (f"ti64micro.batch.step_all (the unmodified reference, baseline/_ref, numba "
+                f"{numba.__version__} threading layer {layer}, n_lanes=8, threads={threads}) on "
+                f"{cpu_model()}")
+        if not args.no_ref_check:  # the oracle on the same windows: bitwise equal states
+            o = orc.HostFields(*[start_state[k] for k in NAMES])
+            orc.advance_points(o, pts, gen, t_start, wins * c["window"], kp, icfg,
+                               threads=threads)
+            check = all(np.array_equal(np.asarray(getattr(rf, k)).view(np.uint8),
+                                       getattr(o, k).view(np.uint8))
+                        for k in ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old"))
+    else:
+        kind = "port"
+        f = orc.HostFields(*[start_state[k] for k in NAMES])
+        secs, wins = cpu_windows(lambda fl: orc.step_all(fl, src.dt, kp, icfg, n_lanes=8,
+                                                         threads=threads),
+                                 f, gen, pts, t_start, c["window"], args.steps, 1e30, threads)
+        desc = (f"oracle/ti64_oracle.c step_all (port; the reference could not be imported: "
+                f"{why}), lanes=8, OpenMP {threads} threads on {cpu_model()}")
+    upd = len(pts) * c["window"] * wins
+    value = upd / secs
+    sample = (f"every {c['stride']}th point of the 2^27 ({len(pts)} points) x {wins} window(s) "
+              f"of {c['window']} steps from step {t_start}: {desc}; T generated outside the "
+              f"timed region; sample state prepared by the oracle in {prep_s:.1f} s")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": wins, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / wins, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "points": 1 << 20,
-                       "note": "CPU: bounded sample of the same job; ms_per_step is the "
-                               "whole 10,000-step job at the sampled rate"},
-            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+            "config": config_dict(cfg_id, args.gpus, args.steps, args.warmup),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "reference_extra": {"jit_seconds": jit_s, "prep_seconds": prep_s,
+                                "timed_seconds": secs,
+                                "ms_per_step_note": "one step = one window of the bounded "
+                                                    "sample (not of all 2^27 points)",
+                                "reference_equals_oracle_bitwise": check}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -272,94 +465,324 @@ def measure_fp64_peak(torch, lib, stream):
     return best
 
 
-def _time_dev(torch, fn, reps=5, flush=None):
-    ts = []
-    for _ in range(reps):
+class Dist:
+    def __init__(self, world, dev):
+        self.world, self.dev = world, dev
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max(self, v):
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_(self, t):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t
+
+
+def measure_ode(torch, pkg, cfg_id, K, W, rank, world, dev, dd, *, counted=True, e2e=True,
+                cpu=True, cpu_budget=10.0, clocks=None, log_prefix=""):
+    """Timed windows of config `cfg_id` on this rank's shard (see module doc).
+    Returns a dict with value / timing / roofline inputs / e2e / cpu leg."""
+    from paper_2402_17580_b200.distributed import shard_range
+    c = CONFIGS[cfg_id]
+    src = pkg.source_for_config(cfg_id)
+    lo, hi = shard_range(c["n"], rank, world)
+    n = hi - lo
+    win = c["window"]
+    stream = torch.cuda.current_stream()
+    scratch = pkg.batch._scratch(n, dev)
+    flush = None
+    if c["n"] * 50 <= (256 << 20):
+        flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    # restart mode: the window is the whole job (configs 0, 1), so every
+    # window re-runs the job from the initial state (restored untimed)
+    restart = win == c["job"]
+    t_prep = time.perf_counter()
+    f = pkg.init_from_source(src, n, point_offset=lo, device=dev)
+    pristine = f.copy() if restart else None
+    s = 0
+    while s < c["start"]:  # untimed preparation, in launches of <= 5000 steps
+        k = min(5000, c["start"] - s)
+        pkg.advance(f, k, src, step0=s, point_offset=lo, scratch=scratch)
+        s += k
+    for _ in range(W):  # warm-up windows (untimed)
+        if restart:
+            _restore(pkg, f, pristine)
+            s = 0
+        pkg.advance(f, win, src, step0=s, point_offset=lo, snapshot_every=win, scratch=scratch)
+        s += win
+    if restart:
+        _restore(pkg, f, pristine)
+        s = 0
+    torch.cuda.synchronize()
+    prep_s = time.perf_counter() - t_prep
+    t_first = s
+    start_copy = f.copy() if (counted or cpu or e2e) else None
+    hist = torch.zeros((3, 256), dtype=torch.int64, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    ev_end = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    sums = None
+    dd.barrier()
+    if clocks is not None:
+        clocks.__enter__()
+    for k in range(K):
+        if restart and k > 0:
+            _restore(pkg, f, pristine)
+            s = 0
         if flush is not None:
             flush.fill_(1.0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fn()
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3)
-    return sorted(ts)[len(ts) // 2]
+        ev[k].record(stream)
+        r = pkg.advance(f, win, src, step0=s, point_offset=lo, snapshot_every=win,
+                        scratch=scratch)
+        launches += r.launches
+        sums = r.sums
+        s += win
+    ev[K].record(stream)
+    # end of the job's timed part: histogram + cross-rank reduction
+    hist.zero_()
+    pkg.histogram(f, 256, out=hist)
+    launches += 1
+    dd.sum_(hist)
+    dd.sum_(sums)
+    ev_end.record(stream)
+    dd.barrier()
+    if clocks is not None:
+        clocks.__exit__(None, None, None)
+    t_windows = [ev[k].elapsed_time(ev[k + 1]) * 1e-3 for k in range(K)]
+    # restart mode restores the state between windows (untimed): the region
+    # is the sum of the windows plus the final reduction
+    t_region = sum(t_windows) + ev[K].elapsed_time(ev_end) * 1e-3
+    t_max = dd.max(t_region)
+    out = {"n_local": n, "lo": lo, "t_region": t_region, "t_max": t_max,
+           "t_windows": t_windows, "launches": launches, "prep_s": prep_s,
+           "first_step": t_first, "value": c["n"] * win * K / t_max,
+           "hist_checksum": int((hist * torch.arange(1, 257, device=dev)).sum().item()),
+           "sums_last": [float(x) for x in sums[-1].cpu().numpy()]}
+    log(f"{log_prefix}config {cfg_id}: {out['value']:.4e} upd/s, "
+        f"{1e3 * sum(t_windows) / K:.2f} ms/window, prep {prep_s:.1f} s")
+    final = f
+    # flop-model totals of the timed windows: the counted instance from the
+    # same starting state; it must reproduce the timed run bit for bit
+    stride = c["stride"]
+    pts_local = np.arange(0, n, stride, dtype=np.int64)
+    sample_after = []
+    if counted:
+        g = start_copy.copy()
+        cnt = pkg.EventCounters(n, dev)
+        s2 = t_first
+        idx = torch.from_numpy(pts_local).to(dev)
+        for k in range(K):
+            if restart and k > 0:
+                _restore(pkg, g, pristine)
+                s2 = 0
+            pkg.advance(g, win, src, step0=s2, point_offset=lo, snapshot_every=win,
+                        counters=cnt, scratch=scratch)
+            s2 += win
+            sample_after.append({k2: getattr(g, k2)[idx].cpu().numpy()
+                                 for k2 in ("x_alpha_s", "x_alpha_m", "x_beta",
+                                            "temperature_old", "seed_active",
+                                            "seed_tracked")})
+        totals = cnt.totals_dict()
+        out["totals"] = totals
+        out["flops"] = flops_from_totals(totals)
+        out["counted_equals_timed"] = all(
+            torch.equal(getattr(g, k2).view(torch.uint8) if getattr(g, k2).dtype != torch.uint8
+                        else getattr(g, k2),
+                        getattr(final, k2).view(torch.uint8) if getattr(final, k2).dtype !=
+                        torch.uint8 else getattr(final, k2))
+            for k2 in pkg.batch.NAMES)
+        del g, cnt
+    # e2e through the public API with the data in pinned host memory
+    if e2e:
+        host = {k: torch.empty(getattr(final, k).shape, dtype=getattr(final, k).dtype,
+                               pin_memory=True) for k in pkg.batch.NAMES}
+        ref = start_copy.copy()
+        pkg.advance(ref, win, src, step0=t_first, point_offset=lo, snapshot_every=win,
+                    scratch=scratch)
+        e2e_t = []
+        same = None
+        for k in range(max(1, min(K, 3))):
+            for k2 in pkg.batch.NAMES:  # fresh inputs on the host, outside the timed region
+                host[k2].copy_(getattr(start_copy, k2))
+            dd.barrier()
+            c0 = time.perf_counter()
+            fh = pkg.GlobalFields(*[host[k2] for k2 in pkg.batch.NAMES], device="host")
+            rh = pkg.advance(fh, win, src, step0=t_first, point_offset=lo, snapshot_every=win,
+                             scratch=scratch)
+            sums_h = rh.sums.cpu()
+            torch.cuda.synchronize()
+            e2e_t.append(time.perf_counter() - c0)
+            if same is None:
+                same = all(torch.equal(host[k2], getattr(ref, k2).cpu())
+                           for k2 in pkg.batch.NAMES)
+        t_e2e = dd.max(statistics.median(e2e_t))
+        h2d = n * (5 * 8 + 2)  # xs, xm, xb, T_old, tracked + 2 flag bytes read
+        d2h = n * (6 * 8 + 2) + sums_h.numel() * 8
+        out["e2e"] = {"value": c["n"] * win / t_e2e, "unit": UNIT,
+                      "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                      "path": "GlobalFields(device='host') + advance(): the fused kernel reads "
+                              "each point's inputs from pinned host memory and writes its "
+                              "results back there (zero-copy), timed to the phase sums on the "
+                              "host", "bitwise_equal_to_device_run": bool(same),
+                      "seconds_per_step": t_e2e}
+        del host, ref
+    # CPU leg: the oracle port on every stride-th point of this shard from the
+    # same starting state; its windows must equal the GPU's bit for bit
+    if cpu and rank == 0 and world == 1:
+        idx = torch.from_numpy(pts_local).to(dev)
+        state = {k2: getattr(start_copy, k2)[idx].cpu().numpy() for k2 in pkg.batch.NAMES}
+        leg = oracle_sample_rate(cfg_id, state, pts_local + lo, t_first, K, cpu_budget)
+        wins = leg["windows"]
+        if sample_after:
+            got = sample_after[wins - 1]
+            fo = leg["fields"]
+            act = got["seed_active"] != 0
+            leg["sample_equals_gpu_bitwise"] = bool(
+                all(np.array_equal(got[k2].view(np.uint8), getattr(fo, k2).view(np.uint8))
+                    for k2 in ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old",
+                               "seed_active")) and
+                np.array_equal(got["seed_tracked"][act].view(np.uint8),
+                               fo.seed_tracked[act].view(np.uint8)))
+        del leg["fields"]
+        out["cpu"] = leg
+    del start_copy, f, final, pristine
+    torch.cuda.empty_cache()
+    return out
 
 
-def measure_extra(torch, pkg, dev):
-    """Secondary evidence (not the headline): the HBM-bound stencil K4 and the
-    fused config-3 step at 512x512x256, config 0 at full size, mid-job
-    windows of the all-active pure-ODE configs 2 and 4 with their FP64
-    roofline, and the Crank-Nicolson step_all (per-GPU, fp64)."""
+def _restore(pkg, dst, src):
+    for k in pkg.batch.NAMES:
+        getattr(dst, k).copy_(getattr(src, k))
+
+
+def roofline_of(m, peak_tf, K):
+    """FP64 roofline of the K2 launches of a measure_ode result (per GPU)."""
+    if "flops" not in m:
+        return None
+    t_launch = sum(m["t_windows"]) / K
+    achieved = m["flops"] / K / t_launch / 1e12
+    return {"bound": "fp64", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": achieved / peak_tf,
+            "flops_per_update": m["flops"] / m["totals"]["point_updates"],
+            "per_launch_s": t_launch}
+
+
+def measure_extra(torch, pkg, dev, dd, peak_tf, args):
+    """Secondary lines (N = 1): config 2 at its full 2^24 points, configs 1
+    and 0 as whole jobs, the whole config-4 job on a 2^21-point shard, the
+    K4 stencil and the split coupled config-3 step at 512x512x256, K1's HBM
+    fraction, and the Crank-Nicolson step_all."""
     from paper_2402_17580_b200 import thermal as th, scanpath
+    out = {}
     hbm = 6538.0
     try:
         hbm = float(json.load(open(ROOT / "MEASURED_PEAKS.json"))["hbm_gbs"])
     except Exception:
         pass
+    # config 2, all 2^24 points, mid-job windows
+    m = measure_ode(torch, pkg, 2, 3, 1, 0, 1, dev, dd, cpu_budget=6.0, log_prefix="extra ")
+    out["config2_full_2^24"] = {
+        "point_updates_per_s": m["value"], "ms_per_window": 1e3 * sum(m["t_windows"]) / 3,
+        "timed_steps": [m["first_step"], m["first_step"] + 3 * CONFIGS[2]["window"]],
+        "roofline": roofline_of(m, peak_tf, 3), "e2e": m.get("e2e"),
+        "cpu_baseline": {k: m["cpu"][k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                   "sample_equals_gpu_bitwise")},
+        "counted_equals_timed_bitwise": m.get("counted_equals_timed")}
+    # configs 1 and 0: one window = the whole job
+    for cid in (1, 0):
+        m = measure_ode(torch, pkg, cid, 3, 1, 0, 1, dev, dd, cpu_budget=5.0,
+                        log_prefix="extra ")
+        rl = roofline_of(m, peak_tf, 3)
+        out[f"config{cid}_whole_job"] = {
+            "point_updates_per_s": m["value"], "ms_per_job": 1e3 * sum(m["t_windows"]) / 3,
+            "algorithmic_flop_rate": rl,
+            "note": "the kernel proves most of these updates exact no-ops (cold idle rest, "
+                    "steady skip) and skips them, so the algorithmic flop rate is not a "
+                    "roofline of executed work" if cid == 1 else
+                    "4096 points = 128 warps: latency-bound by size",
+            "e2e": m.get("e2e"),
+            "cpu_baseline": {k: m["cpu"][k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                       "sample_equals_gpu_bitwise")}}
+    # whole config-4 job on a 2^21-point shard (per-window rates vs the job)
+    src4 = pkg.source_for_config(4)
+    nsh = 1 << 21
+    f4 = pkg.init_from_source(src4, nsh, device=dev)
+    scr = pkg.batch._scratch(nsh, dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pkg.advance(f4, CONFIGS[4]["job"], src4, scratch=scr, snapshot_every=1000)
+    e1.record()
+    e1.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    out["config4_whole_job_2^21_shard"] = {"point_updates_per_s": nsh * CONFIGS[4]["job"] / t,
+                                           "seconds": t}
+    del f4, scr
+    # config 3: K4 and the split coupled step
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
-    out = {}
     nz, ny, nx = 256, 512, 512
     n = nz * ny * nx
     dom = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=20e-6, device=dev)
-    src = th.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=20e-6)
+    srcb = th.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=20e-6)
     segs = scanpath.serpentine((1e-3, 1e-3, 9.24e-3, 9.24e-3), 80e-6, 1.0, 0.35 * 250.0)
     beams = scanpath.beam_schedule(segs, 400, 1e-6)
-    dom.run(100, 1e-6, beams, src, fused=True)
+    dom.run(100, 1e-6, beams, srcb, fused=True)
     k = [100]
 
-    # 10 back-to-back steps per timed region (1 GiB per step >> L2, so no
-    # flush is needed): the host enqueues ahead of the device, so the launch
-    # overhead of the Python call does not show up as device idle time
+    def timed(fn, reps):
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        return sorted(ts)[len(ts) // 2]
+
     def stencil():
         for _ in range(10):
-            th.step_thermal(dom.field, 1e-6, th.DEFAULT_THERMAL, src, beams[k[0]], losses=False,
+            th.step_thermal(dom.field, 1e-6, th.DEFAULT_THERMAL, srcb, beams[k[0]], losses=False,
                             bottom_dirichlet=353.0, all_built=True)
-    t = _time_dev(torch, stencil, 5) / 10
+    t = timed(stencil, 5) / 10
     out["stencil_K4_config3_grid"] = {
-        "cells": n, "us": t * 1e6, "GB/s": 16 * n / t / 1e9, "frac_of_measured_hbm": 16 * n / t / 1e9 / hbm,
+        "cells": n, "us": t * 1e6, "GB/s": 16 * n / t / 1e9,
+        "frac_of_measured_hbm": 16 * n / t / 1e9 / hbm,
         "bytes_model": "16 B/cell (8 read T_n + 8 write T_n+1)", "pipeline": "TMA + mbarrier ring",
         "timing": "10 consecutive steps per event pair (inputs 1 GiB > L2)"}
 
     def coupled():
-        dom.run(10, 1e-6, beams[k[0]:], src, fused=True)
+        dom.run(10, 1e-6, beams[k[0]:], srcb, fused=True)
         k[0] += 10
-    t = _time_dev(torch, coupled, 5) / 10
-    out["config3_coupled_step"] = {"cells": n, "ms_per_step": t * 1e3,
-                                   "cell_steps_per_s": n / t,
-                                   "job_estimate_s": 20000 * t,
+    t = timed(coupled, 5) / 10
+    out["config3_coupled_step"] = {"cells": n, "ms_per_step": t * 1e3, "cell_steps_per_s": n / t,
                                    "path": "split: K4 + hot-row bitmap, row scan, kinetics of "
-                                           "listed rows (early in the job: few transformed rows)"}
-    del dom
-    # config 0 at its full size (4096 points x 20 000 steps, one launch)
-    src0 = pkg.source_for_config(0)
-    f0 = pkg.init_from_source(src0, 4096, device=dev)
-    pkg.advance(f0.copy(), 20000, src0, snapshot_every=1000)
-    t = _time_dev(torch, lambda: pkg.advance(f0.copy(), 20000, src0, snapshot_every=1000), 3)
-    out["config0_full_4096x20000"] = {"point_updates_per_s": 4096 * 20000 / t, "ms": t * 1e3,
-                                      "note": "128 warps on 148 SMs: latency-bound by size"}
-    # the all-active pure-ODE configs: a mid-job window of 2000 steps on a
-    # per-GPU shard, from the state the job has reached there (config 2 at
-    # step 10 000 of 50 000 with 2^22 points, config 4 at step 50 000 of
-    # 100 000 with 2^21 points); every point transforms every step.  F from
-    # one counted run of the same window (the headline's flop model).
-    for c, nsh, s0 in ((2, 1 << 22, 10000), (4, 1 << 21, 50000)):
-        src_c = pkg.source_for_config(c)
-        f = pkg.init_from_source(src_c, nsh, device=dev)
-        pkg.advance(f, s0, src_c)
-        cnt = pkg.EventCounters(nsh, dev)
-        pkg.advance(f.copy(), 2000, src_c, step0=s0, counters=cnt)
-        fl = flops_from_totals(cnt.totals_dict())
-        t = _time_dev(torch, lambda: pkg.advance(f.copy(), 2000, src_c, step0=s0), 3)
-        rate = nsh * 2000 / t
-        out[f"config{c}_shard_2^{nsh.bit_length() - 1}_steps_{s0}-{s0 + 2000}"] = {
-            "point_updates_per_s": rate, "ms": t * 1e3,
-            "flops_per_update": fl / (nsh * 2000), "TFLOP/s": fl / t / 1e12,
-            "job_estimate_s_per_gpu": {2: (1 << 24) * 50000, 4: (1 << 24) * 100000}[c] / rate,
-            "job_note": "config 2: full 2^24-point job on one GPU; config 4: the 2^24-point "
-                        "per-GPU shard of the 8-GPU job"}
+                                           "listed rows (early in the job)"}
+    del dom, flush
+    # K1 (one step_all) at 2^26 cold points: the HBM-bound per-step kernel
+    n1 = 1 << 26
+    f1 = pkg.GlobalFields.allocate(n1, temperature=300.0, device=dev)
+    f1.x_alpha_s.fill_(0.9)
+    f1.x_beta.fill_(0.1)
+    pkg.step_all(f1, 1e-5)
+    t = timed(lambda: pkg.step_all(f1, 1e-5), 5)
+    out["K1_step_all_2^26"] = {"ms": t * 1e3, "GB/s": 73 * n1 / t / 1e9,
+                               "frac_of_measured_hbm": 73 * n1 / t / 1e9 / hbm,
+                               "bytes_model": "73 B/point-update (72 model + 1 seed flag)"}
+    del f1
     # Crank-Nicolson step_all on the reference's block-100 benchmark layout
-    # (bench.py:131-155: dt = dt_sub_max = 0.01), its analytic flop count
     cfg = pkg.IntegratorConfig(scheme="crank_nicolson", dt_sub_max=0.01)
     n = 1 << 22
     lay = branch_layout(100, n)
@@ -369,18 +792,18 @@ def measure_extra(torch, pkg, dev):
     work = [pristine.copy() for _ in range(5)]
     ts = []
     for w in work:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         pkg.step_all(w, 0.01, config=cfg, n_lanes=8)
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3)
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
     t = sorted(ts)[len(ts) // 2]
     fl = reference_flops(lay[0], lay[1], lay[3], lay[4], 8, "crank_nicolson", mean_it)
     out["crank_nicolson_layout_block100_2^22"] = {
-        "point_updates_per_s": n / t, "GDoF_per_s": 3 * n / t / 1e9, "ms": t * 1e3,
-        "mean_fixed_point_iters": mean_it, "reference_flops_per_point": fl / n,
-        "TFLOP/s": fl / t / 1e12, "note": "includes the per-call failure readback (sync)"}
+        "point_updates_per_s": n / t, "ms": t * 1e3, "mean_fixed_point_iters": mean_it,
+        "reference_flops_per_point": fl / n, "TFLOP/s": fl / t / 1e12,
+        "frac_of_fp64_peak": fl / t / 1e12 / peak_tf}
     return out
 
 
@@ -391,170 +814,59 @@ def run_b200(args):
     from paper_2402_17580_b200 import _lib
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    lib = _lib.require()
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.require()
+    dd = Dist(world, dev)
     stream = torch.cuda.current_stream()
-    src = pkg.source_for_config(1)
-    n = src.n_points
-    nsteps = args.job_steps
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
-    pristine = pkg.init_from_source(src, n, device=dev)
-    work = pristine.copy()
-    scratch = pkg.batch._scratch(n, dev)
-
-    def one_job(fields, counters=None):
-        return pkg.advance(fields, nsteps, src, snapshot_every=SNAP_EVERY,
-                           counters=counters, scratch=scratch)
-
-    # warm-up
-    for _ in range(args.warmup):
-        for k in pkg.batch.NAMES:
-            getattr(work, k).copy_(getattr(pristine, k))
-        one_job(work)
-    torch.cuda.synchronize()
-
-    # flop model totals of the job (deterministic; one counted run, untimed)
-    for k in pkg.batch.NAMES:
-        getattr(work, k).copy_(getattr(pristine, k))
-    cnt = pkg.EventCounters(n, dev)
-    one_job(work, cnt)
-    totals = cnt.totals_dict()
-    flops_job = flops_from_totals(totals)
-    counted_state = work.to_host()
-
-    # timed region
-    times = []
-    launches = 0
-    sums_last = None
-    with ClockSampler(local) as clk:
-        barrier()
-        for _ in range(args.steps):
-            for k in pkg.batch.NAMES:
-                getattr(work, k).copy_(getattr(pristine, k))
-            flush.fill_(1.0)  # > L2: evict the previous job's state
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            r = one_job(work)
-            e1.record(stream)
-            launches += r.launches
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1) * 1e-3)
-            sums_last = r.sums
-        barrier()
-    # uncounted timed run must reproduce the counted run bit for bit
-    same = all(np.array_equal(work.host(k), counted_state[k]) for k in pkg.batch.NAMES)
-    total_s = sum(times)
-    t_max = torch.tensor([total_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        # final global phase-fraction reduction (the path's only exchange)
-        dist.all_reduce(sums_last, op=dist.ReduceOp.SUM)
-    total_s = float(t_max.item())
-    upd_job = n * nsteps
-    value = world * upd_job * args.steps / total_s
-
-    # e2e through the public API with the data on the host (pinned): the
-    # fused kernel reads every point's inputs from host memory and writes its
-    # results back itself (zero-copy, GlobalFields(device="host")), so the
-    # host-link transfer overlaps the computation; timed to the results
-    # being readable on the host (device sync + the snapshot sums D2H)
-    host = {k: torch.from_numpy(pristine.host(k)).pin_memory() for k in pkg.batch.NAMES}
-    work_h = {k: torch.empty_like(v).pin_memory() for k, v in host.items()}
-    read_names = ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old", "seed_tracked",
-                  "seed_active", "seed_direction")
-    h2d = sum(host[k].numel() * host[k].element_size() for k in read_names)
-    d2h = sum(v.numel() * v.element_size() for v in host.values())
-    e2e_times = []
-    for _ in range(max(1, min(args.steps, 3))):
-        for k in pkg.batch.NAMES:  # fresh inputs, outside the timed region
-            work_h[k].copy_(host[k])
-        barrier()
-        t0 = time.perf_counter()
-        f = pkg.GlobalFields(*[work_h[k] for k in pkg.batch.NAMES], device="host")
-        r_h = pkg.advance(f, nsteps, src, snapshot_every=SNAP_EVERY, scratch=scratch)
-        sums_h = r_h.sums.cpu()
-        torch.cuda.synchronize()
-        e2e_times.append(time.perf_counter() - t0)
-    d2h += sums_h.numel() * sums_h.element_size()
-    e2e_same = all(np.array_equal(work_h[k].numpy(), counted_state[k]) for k in pkg.batch.NAMES)
-    e2e_t = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * upd_job / float(e2e_t.item())
-    # the explicit-copy variant (H2D, device-resident advance, D2H states)
-    out_host = torch.empty((n, 3), dtype=torch.float64).pin_memory()
-    cp_times = []
-    for _ in range(max(1, min(args.steps, 3))):
-        barrier()
-        t0 = time.perf_counter()
-        f = pkg.GlobalFields(*[host[k] for k in pkg.batch.NAMES], device=dev)
-        pkg.advance(f, nsteps, src, snapshot_every=SNAP_EVERY, scratch=scratch)
-        f.states(out=out_host)
-        torch.cuda.synchronize()
-        cp_times.append(time.perf_counter() - t0)
-    e2e_copy_value = world * upd_job / statistics.median(cp_times)
-
-    extra = measure_extra(torch, pkg, dev) if (rank == 0 and not args.quick) else None
+    peak = measure_fp64_peak(torch, lib, stream) / 1e12
+    clk = ClockSampler(local)
+    K, W = args.steps, args.warmup
+    m = measure_ode(torch, pkg, HEADLINE, K, W, rank, world, dev, dd, clocks=clk,
+                    cpu=not args.no_cpu_baseline, cpu_budget=args.cpu_budget)
+    extra = None
+    if world == 1 and not args.quick:
+        extra = measure_extra(torch, pkg, dev, dd, peak, args)
+    rl = roofline_of(m, peak, K)
+    if rl is not None:
+        rl.update({"peak_source": "measured on this box: DFMA stream (ti64_bench_dfma); "
+                                  "MEASURED_PEAKS.json has no FP64 entry",
+                   "kernel": "advance_kernel<PULSE_SWEEP> (K2), one launch per window",
+                   "traffic": K2_PROFILE["dram_bytes_per_launch"],
+                   "traffic_source": K2_PROFILE["file"],
+                   "executed": {k: K2_PROFILE[k] for k in ("fp64_pipe_active", "issue_active")},
+                   "note": "achieved = the reference's flop model (SURVEY 8d F, from the "
+                           "kernel's own branch counters over the timed windows) / mean "
+                           "launch time; per GPU"})
     if rank == 0:
-        peak = measure_fp64_peak(torch, lib, stream)
-        adv_per_job = max(1, r.launches // 2)  # advance + snapshot-sum kernel pairs
-        per_launch_s = total_s / (args.steps * adv_per_job)
-        flops_launch = flops_job / adv_per_job
-        achieved = flops_launch / per_launch_s / 1e12
-        peak_tf = peak / 1e12
-        for v in (extra or {}).values():
-            if isinstance(v, dict) and "TFLOP/s" in v:
-                v["frac_of_fp64_peak"] = v["TFLOP/s"] / peak_tf
-        cpu = None if args.no_cpu_baseline else cpu_reference(budget_s=args.cpu_budget)
-        clocks = clk.summary()
+        c = CONFIGS[HEADLINE]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "points_per_gpu": n, "job_steps": nsteps,
-                       "snapshot_every": SNAP_EVERY,
-                       "l2": "flushed between timed iterations (256 MiB write)",
-                       "parallelism": f"points sharded, {world} replica(s) of the job"},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf,
-                         "unit": "TFLOP/s", "frac": achieved / peak_tf,
-                         "traffic": K2_JOB_DRAM_BYTES,
-                         "traffic_source": "ncu --set full of this job's K2 launch "
-                                           "(profiles/r01b_advance_cfg1_job.txt): "
-                                           "dram read + write bytes per launch",
-                         "peak_source": "measured on this box: DFMA stream (ti64_bench_dfma)",
-                         "flops_per_update": flops_job / upd_job,
-                         "kernel": "advance_kernel<ROSENTHAL>",
-                         "executed": K2_JOB_EXECUTED,
-                         "note": "achieved credits the reference's flops (SURVEY 8d F) to every "
-                                 "point-update; the kernel proves most config-1 updates exact "
-                                 "no-ops and skips them, hence frac > 1. What the FP64 pipe "
-                                 "executes is 'executed'; the all-active configs 2/4 in 'extra' "
-                                 "are the compute-bound view"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "path": "GlobalFields(device='host') + advance: zero-copy, the kernel "
-                            "reads inputs from / writes results to pinned host memory",
-                    "bitwise_equal_to_device_run": bool(e2e_same),
-                    "explicit_copy_value": e2e_copy_value},
-            "gpu_launches": launches,
-            "clocks": clocks,
-            "cpu_baseline": None if cpu is None else
-            {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": 1e3 * m["t_max"] / K,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": config_dict(HEADLINE, world, K, W),
+            "roofline": rl,
+            "e2e": m.get("e2e"),
+            "gpu_launches": m["launches"],
+            "clocks": clk.summary(),
+            "cpu_baseline": None if "cpu" not in m else
+            {k: m["cpu"][k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "checks": {"counted_equals_timed_bitwise": m.get("counted_equals_timed"),
+                       "cpu_sample_equals_gpu_bitwise":
+                           m.get("cpu", {}).get("sample_equals_gpu_bitwise"),
+                       "e2e_equals_device_bitwise":
+                           (m.get("e2e") or {}).get("bitwise_equal_to_device_run"),
+                       "totals": m.get("totals"), "sums_last": m["sums_last"],
+                       "hist_checksum": m["hist_checksum"]},
+            "timing": {"prep_seconds": m["prep_s"], "window_seconds": m["t_windows"],
+                       "points_per_gpu": m["n_local"],
+                       "job_estimate_seconds": m["t_max"] / K * c["job"] / c["window"]},
             "extra": extra,
-            "checks": {"counted_equals_timed_bitwise": bool(same),
-                       "sums_last": [float(x) for x in sums_last[-1].cpu().numpy()],
-                       "totals": totals},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -563,17 +875,53 @@ def run_b200(args):
     return 0
 
 
+def run_plumbing_test(args):
+    """CPU (gloo) check of the multi-rank plumbing the GPU arm uses: spawn,
+    shard tiling, sum/max all-reduce.  Prints one JSON line on rank 0."""
+    import torch
+    import torch.distributed as dist
+    from paper_2402_17580_b200.distributed import shard_range
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    n = CONFIGS[HEADLINE]["n"]
+    lo, hi = shard_range(n, rank, world)
+    t = torch.tensor([float(hi - lo), float(rank + 1)], dtype=torch.float64)
+    mx = torch.tensor([float(rank)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    bounds = [shard_range(n, r, world) for r in range(world)]
+    if rank == 0:
+        print(json.dumps({"plumbing_test": True, "n_gpus": world, "shards": bounds,
+                          "points_sum": t[0].item(), "rank_sum": t[1].item(),
+                          "max_rank": mx.item()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--job-steps", type=int, default=JOB_STEPS)
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ref-check", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the secondary measurements")
-    args = ap.parse_args()
+    ap.add_argument("--plumbing-test", action="store_true", help=argparse.SUPPRESS)
+    argv = sys.argv[1:]
+    args = ap.parse_args(argv)
+    if args.warmup < 0 or args.steps < 1:
+        raise SystemExit("need --steps >= 1 and --warmup >= 0")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus, argv)
+    if args.plumbing_test:
+        return run_plumbing_test(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_b200(args)

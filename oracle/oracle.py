@@ -71,6 +71,8 @@ def lib():
         L.oracle_advance.restype = I64
         L.oracle_advance_points.argtypes = [P, P, I64, P, I64, I64, I64, P, P, P, P, P, I32]
         L.oracle_advance_points.restype = I64
+        L.oracle_gen_temperature_points.argtypes = [P, P, I64, I64, I64, P, I32]
+        L.oracle_gen_temperature_points.restype = None
         L.oracle_history.argtypes = [P, P, I64, D, D, D, P, P, P]
         L.oracle_history.restype = I64
         L.oracle_stencil_step.argtypes = [P, P, P, P, P, P]
@@ -247,6 +249,17 @@ def advance_points(fields, points, gen, step0, nsteps, kp, cfg, threads=None, ns
     if rc != 0:
         raise RuntimeError(f"oracle_advance_points rc={rc}")
     return {"martensite": mart, "switches": sw, "totals": totals}
+
+
+def gen_temperature_points(gen, points, step0, nsteps, threads=None):
+    """(nsteps, m) temperatures of GLOBAL points at steps step0.. (K3's
+    definition)."""
+    pts = np.ascontiguousarray(points, dtype=np.int64)
+    out = np.empty((int(nsteps), len(pts)))
+    threads = max_threads() if threads is None else threads
+    lib().oracle_gen_temperature_points(C.byref(gen), _p(pts), len(pts), int(step0),
+                                        int(nsteps), _p(out), int(threads))
+    return out
 
 
 def gen_initial_points(gen, points):

@@ -725,6 +725,22 @@ double oracle_gen_temperature1(const ti64_tempgen* g, int64_t local, int64_t ste
   return pointgen_temp(g, &q, step);
 }
 
+/* T at steps step0 .. step0+nsteps-1 of the points with GLOBAL indices
+ * pts[0..m): out is (nsteps, m) row-major (the CPU legs' inputs, generated
+ * outside their timed regions). */
+void oracle_gen_temperature_points(const ti64_tempgen* g, const int64_t* pts, int64_t m,
+                                   int64_t step0, int64_t nsteps, double* out,
+                                   int32_t threads) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(threads > 0 ? threads : 1)
+#endif
+  for (int64_t j = 0; j < m; ++j) {
+    pointgen q;
+    pointgen_init(g, (uint64_t)pts[j], &q);
+    for (int64_t s = 0; s < nsteps; ++s) out[s * m + j] = pointgen_temp(g, &q, step0 + s);
+  }
+}
+
 void oracle_gen_temperature(const ti64_tempgen* g, int64_t n, int64_t step, double* out,
                             int32_t threads) {
 #ifdef _OPENMP
@@ -840,12 +856,15 @@ int64_t oracle_advance(const ti64_fields* f, int64_t n, const ti64_tempgen* g,
 }
 
 /* The reference loop of oracle_advance for a SUBSET of points given by their
- * GLOBAL indices pts[0..m) (e.g. every 1024th point of a config): points are
- * independent, so each runs alone as a width-1 lane batch (explicit-scheme
- * states are lane-width invariant, test_batch.py:79-85; the seed arrays of
- * inactive points are lane-width-dependent residue and are not compared).
+ * GLOBAL indices pts[0..m) (e.g. every 1024th point of a config).  Points are
+ * independent: consecutive subset points are grouped into lane batches of 8
+ * (the reference's default width) and each group runs the whole loop alone;
+ * explicit-scheme states are lane-width and batch-composition invariant
+ * (test_batch.py:79-85), while the seed arrays of INACTIVE points are
+ * batch-dependent residue (batch.py:687-692) and are not compared.
  * f holds the m points' state (in/out); counters as oracle_advance
  * (per-point mart/sw may be NULL; totals[8] may be NULL). */
+#define AP_LANES 8
 int64_t oracle_advance_points(const ti64_fields* f, const int64_t* pts, int64_t m,
                               const ti64_tempgen* g, int64_t step0, int64_t nsteps,
                               int64_t nsub, const ti64_kparams* kp, const ti64_icfg* cfg,
@@ -854,45 +873,76 @@ int64_t oracle_advance_points(const ti64_fields* f, const int64_t* pts, int64_t 
   int64_t rc_all = 0;
   uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, t6 = 0, t7 = 0;
   const double dt_sub = g->dt / (double)nsub;
+  const int64_t ngroups = (m + AP_LANES - 1) / AP_LANES;
 #ifdef _OPENMP
-#pragma omp parallel for schedule(dynamic, 16) num_threads(threads > 0 ? threads : 1) \
+#pragma omp parallel for schedule(dynamic, 4) num_threads(threads > 0 ? threads : 1) \
     reduction(max : rc_all) reduction(+ : t0, t1, t2, t3, t4, t5, t6, t7)
 #endif
-  for (int64_t j = 0; j < m; ++j) {
-    pointgen q;
-    pointgen_init(g, (uint64_t)pts[j], &q);
-    ti64_fields fj = {f->x_alpha_s + j,    f->x_alpha_m + j,    f->x_beta + j,
-                      f->temperature_old + j, f->temperature_new + j, f->seed_tracked + j,
-                      f->seed_active + j,  f->seed_direction + j};
-    uint32_t mc = 0, sc = 0;
-    for (int64_t s = 0; s < nsteps; ++s) {
-      const double T1 = pointgen_temp(g, &q, step0 + s + 1);
-      f->temperature_new[j] = T1;
-      const double xs = f->x_alpha_s[j], xm = f->x_alpha_m[j];
-      const double xa = xs + xm;
-      const double xe0 = xaeq_of(f->temperature_old[j], kp);
-      const int grow = (xa < xe0) & (xs > 0.0);
-      const int am = (xm > 0.0) & (xs > 0.0);
-      const int dis = (xa > xe0) & (xa < XA_MAX);
-      t1 += T1 < kp->t_am_start;
-      t2 += grow | am;
-      t3 += grow;
-      t4 += am;
-      t5 += dis;
-      const int amx = argmax3(xs, xm, f->x_beta[j]);
-      int64_t rc = oracle_run_range(&fj, 0, 1, 1, nsub, dt_sub, kp, cfg);
-      if (rc != 0) {
-        if (rc_all < j + 1) rc_all = j + 1;
-        break;
-      }
-      mc += f->x_alpha_m[j] > xm;
-      sc += argmax3(f->x_alpha_s[j], f->x_alpha_m[j], f->x_beta[j]) != amx;
+  for (int64_t gi = 0; gi < ngroups; ++gi) {
+    const int64_t j0 = gi * AP_LANES;
+    const int w = (int)(m - j0 < AP_LANES ? m - j0 : AP_LANES);
+    pointgen q[AP_LANES];
+    double xs[AP_LANES], xm[AP_LANES], xb[AP_LANES], to[AP_LANES], tn[AP_LANES], tr[AP_LANES];
+    uint8_t ac[AP_LANES], dr[AP_LANES];
+    uint32_t mc[AP_LANES] = {0}, sc[AP_LANES] = {0};
+    for (int l = 0; l < w; ++l) {
+      const int64_t j = j0 + l;
+      pointgen_init(g, (uint64_t)pts[j], &q[l]);
+      xs[l] = f->x_alpha_s[j];
+      xm[l] = f->x_alpha_m[j];
+      xb[l] = f->x_beta[j];
+      to[l] = f->temperature_old[j];
+      tn[l] = f->temperature_new[j];
+      tr[l] = f->seed_tracked[j];
+      ac[l] = f->seed_active[j];
+      dr[l] = f->seed_direction[j];
     }
-    if (mart) mart[j] += mc;
-    if (sw) sw[j] += sc;
-    t0 += (uint64_t)nsteps;
-    t6 += mc;
-    t7 += sc;
+    ti64_fields fg = {xs, xm, xb, to, tn, tr, ac, dr};
+    int failed = 0;
+    for (int64_t s = 0; s < nsteps && !failed; ++s) {
+      double xm_prev[AP_LANES];
+      int am_prev[AP_LANES];
+      for (int l = 0; l < w; ++l) {
+        tn[l] = pointgen_temp(g, &q[l], step0 + s + 1);
+        const double xa = xs[l] + xm[l];
+        const double xe0 = xaeq_of(to[l], kp);
+        const int grow = (xa < xe0) & (xs[l] > 0.0);
+        const int am = (xm[l] > 0.0) & (xs[l] > 0.0);
+        const int dis = (xa > xe0) & (xa < XA_MAX);
+        t1 += tn[l] < kp->t_am_start;
+        t2 += grow | am;
+        t3 += grow;
+        t4 += am;
+        t5 += dis;
+        xm_prev[l] = xm[l];
+        am_prev[l] = argmax3(xs[l], xm[l], xb[l]);
+      }
+      const int64_t rc = oracle_run_range(&fg, 0, w, AP_LANES, nsub, dt_sub, kp, cfg);
+      if (rc != 0) {
+        if (rc_all < j0 + rc) rc_all = j0 + rc;
+        failed = 1;
+      }
+      for (int l = 0; l < w; ++l) {
+        mc[l] += xm[l] > xm_prev[l];
+        sc[l] += argmax3(xs[l], xm[l], xb[l]) != am_prev[l];
+      }
+    }
+    for (int l = 0; l < w; ++l) {
+      const int64_t j = j0 + l;
+      f->x_alpha_s[j] = xs[l];
+      f->x_alpha_m[j] = xm[l];
+      f->x_beta[j] = xb[l];
+      f->temperature_old[j] = to[l];
+      f->temperature_new[j] = tn[l];
+      f->seed_tracked[j] = tr[l];
+      f->seed_active[j] = ac[l];
+      f->seed_direction[j] = dr[l];
+      if (mart) mart[j] += mc[l];
+      if (sw) sw[j] += sc[l];
+      t6 += mc[l];
+      t7 += sc[l];
+    }
+    t0 += (uint64_t)nsteps * (uint64_t)w;
   }
   if (totals) {
     totals[0] += t0;
@@ -955,6 +1005,11 @@ void oracle_stencil_step(const double* src, double* dst, double* rc,
   double inv_rc = a->dt / tp->rho_c;
   double dk = tp->k_ms - tp->k_p;
   double t4inf = pow(tp->t_inf, 4.0);
+  /* every cell writes only its own dst entry: planes run in parallel (the
+   * reference's serial loop order does not affect any result) */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
   for (int64_t z = a->z_begin; z < a->z_end; ++z)
     for (int64_t y = 0; y < ny; ++y)
       for (int64_t x = 0; x < nx; ++x) {
@@ -1012,6 +1067,9 @@ void oracle_stencil_step(const double* src, double* dst, double* rc,
     for (int64_t y = 0; y < ny; ++y)
       for (int64_t x = 0; x < nx; ++x)
         if (state[IDX(0, y, x)] != STATE_INACTIVE) dst[IDX(0, y, x)] = a->bc_bottom;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
   for (int64_t z = a->z_begin; z < a->z_end; ++z)
     for (int64_t y = 0; y < ny; ++y)
       for (int64_t x = 0; x < nx; ++x)

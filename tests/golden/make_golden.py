@@ -649,7 +649,51 @@ def make_initiation():
     np.savez_compressed(OUT / "initiation.npz", **c)
 
 
+def _digest(f):
+    import hashlib
+    out = {}
+    act = np.asarray(f.seed_active) != 0
+    for k in ("x_alpha_s", "x_alpha_m", "x_beta", "temperature_old", "seed_active"):
+        out[k] = hashlib.sha256(np.ascontiguousarray(getattr(f, k)).tobytes()).hexdigest()
+    out["seed_tracked_active"] = hashlib.sha256(
+        np.ascontiguousarray(np.asarray(f.seed_tracked)[act]).tobytes()).hexdigest()
+    return out
+
+
+def make_advance_large():
+    """Large reference runs that select the fused kernel's throughput
+    instance (> 37 888 points, > 1184 32-point tasks): the final state's
+    SHA-256 per array (seed_tracked only where active) and the first 4096
+    points in full.  Reference step_all (n_lanes=8) with this project's
+    generators (oracle definitions), threads=all."""
+    cases = {"cfg4_40960_off3x2^24_0-24000": (4, 40960, 3 << 24, 24000),
+             "cfg2_65536_off0_0-6000": (2, 65536, 0, 6000)}
+    out = {}
+    threads = os.cpu_count() or 1
+    for name, (cfg_id, n, off, nsteps) in cases.items():
+        src = sources.source_for_config(cfg_id)
+        gen = src.tempgen(point_offset=off)
+        init = orc.gen_initial_state(gen, n)
+        t0 = orc.gen_temperature(gen, n, 0, threads)
+        f = GlobalFields(init.x_alpha_s, init.x_alpha_m, init.x_beta, t0, t0.copy())
+        for s in range(nsteps):
+            f.temperature_new[:] = orc.gen_temperature(gen, n, s + 1, threads)
+            step_all(f, src.dt, DEFAULT_PARAMS, CFG_E, n_lanes=8, threads=threads)
+        d = _digest(f)
+        out[f"{name}/args"] = np.array([cfg_id, n, off, nsteps], np.int64)
+        for k, v in d.items():
+            out[f"{name}/sha_{k}"] = np.array(v)
+        for k in NAMES:
+            out[f"{name}/head_{k}"] = np.array(getattr(f, k))[:4096]
+        print(name, d["x_alpha_s"][:16], flush=True)
+    np.savez_compressed(OUT / "advance_large.npz", **out)
+
+
 if __name__ == "__main__":
+    if "--large-only" in sys.argv:
+        make_advance_large()
+        print("advance large done")
+        sys.exit(0)
     if "--init-only" in sys.argv:
         make_initiation()
         print("initiation done")
