@@ -6,9 +6,10 @@
 // so a point's history does not depend on sharding or launch shape.
 //
 // Pulse sums skip pulses whose contribution is provably an exact no-op:
-// outside a conservative step window around its centre u^2 > 45, so
-// A*fast_exp(-u^2) < 1e-16 while the running sum is >= base >= 256, whose
-// half-ulp is 2^-45 ~ 2.8e-14 — adding it cannot change a bit.
+// outside a conservative step window |t - t_c| > wk w around its centre,
+// A*fast_exp(-u^2) < ulp(base)/2 <= ulp(running sum)/2 (every term is >= 0),
+// so adding it cannot change a bit (wk from the amplitude
+// bound and the base, pulse_window_k in ti64_kernels.cu).
 #pragma once
 #include "ti64_fastmath.cuh"
 #include "../../include/ti64_b200.h"
@@ -80,13 +81,16 @@ struct PulseSet {
   double ca, ctc, ciw;
 #endif
 
-  __device__ __forceinline__ void add(int k, double ak, double tck, double w, double dt) {
+  // wk (> 0): half-width of the live window in widths, from the host
+  // (pulse_window_k): outside it a*fast_exp(-u^2) < ulp(base)/2, an exact no-op
+  __device__ __forceinline__ void add(int k, double ak, double tck, double w, double dt,
+                                      double wk) {
     a[k] = ak;
     tc[k] = tck;
     inv_w[k] = div_rn(1.0, w);
-    // conservative window: outside it |t - tc| >= 7w - O(ulp) => u^2 > 45
-    const double l = floor((tck - 7.0 * w) / dt) - 2.0;
-    const double h = ceil((tck + 7.0 * w) / dt) + 2.0;
+    // conservative window: outside it |t - tc| >= wk w - O(ulp) (2-step margin)
+    const double l = floor((tck - wk * w) / dt) - 2.0;
+    const double h = ceil((tck + wk * w) / dt) + 2.0;
     lo[k] = l < -1.0e9 ? -1000000000 : (l > 1.0e9 ? 1000000000 : (int)l);
     hi[k] = h < -1.0e9 ? -1000000000 : (h > 1.0e9 ? 1000000000 : (int)h);
   }
@@ -156,6 +160,14 @@ struct PulseSet {
   }
 };
 
+// live-window half-width of the pulse kinds (g.pf[7], set by the library's
+// entry points from pulse_window_k); 26.7 (u^2 > 708: fast_exp is exactly 0)
+// is exact for any base and amplitude
+__device__ __forceinline__ double window_k(const ti64_tempgen& g) {
+  const double k = (double)g.pf[7];
+  return k > 0.0 ? k : 26.7;
+}
+
 // config 0 (TI64_SRC_PULSE): p = {A_lo, A_hi, tc_lo, tc_hi, w_lo, w_hi}
 template <int MAXP>
 __device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempgen& g,
@@ -165,7 +177,7 @@ __device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempg
   const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
   const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 1));
   const double w = unif(g.p[4], g.p[5], u01(g.seed, pt, 2));
-  ps.add(0, a, tc, w, g.dt);
+  ps.add(0, a, tc, w, g.dt, window_k(g));
   ps.next_event = -1;
   ps.live = 0u;
 }
@@ -184,7 +196,7 @@ __device__ __forceinline__ void init_train(PulseSet<MAXP>& ps, const ti64_tempge
     const double tc = __dadd_rn(__dadd_rn(g.p[4], __dmul_rn(g.p[5], (double)k)),
                                 unif(g.p[6], g.p[7], u01(g.seed, pt, 2 + 3 * k)));
     const double w = unif(g.p[8], g.p[9], u01(g.seed, pt, 3 + 3 * k));
-    ps.add(k, a, tc, w, g.dt);
+    ps.add(k, a, tc, w, g.dt, window_k(g));
     scale = __dmul_rn(scale, g.p[10]);
   }
   ps.next_event = -1;
@@ -202,7 +214,7 @@ __device__ __forceinline__ void init_sweep(PulseSet<MAXP>& ps, const ti64_tempge
     const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 1 + 3 * k));
     const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 2 + 3 * k));
     const double w = fast_exp(unif(g.p[4], g.p[5], u01(g.seed, pt, 3 + 3 * k)));
-    ps.add(k, a, tc, w, g.dt);
+    ps.add(k, a, tc, w, g.dt, window_k(g));
   }
   ps.next_event = -1;
   ps.live = 0u;

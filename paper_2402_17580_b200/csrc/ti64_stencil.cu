@@ -157,6 +157,10 @@ struct CoupledODE {
   int L;
   int rest_ok;  // t_as_end <= t_sol etc.: the cold idle rest is exact
   uint32_t* hot;  // split mode: 1 bit per 32-cell row, set where T_n or T_n+1 >= t_as_end
+  // slab form: the kinetics state (fields, idle bits, hot rows) starts at
+  // global plane sz0; toff = (sz0 - z_base) * plane maps a state index to
+  // the temperature arrays (which hold planes from z_base)
+  int64_t sz0, toff;
 };
 
 // ---------------------------------------------------------------------------
@@ -277,20 +281,23 @@ __device__ __forceinline__ void cell_kinetics(const ti64_fields& f, uint32_t* __
 // clears the hot bits; rows_kinetics_kernel runs one listed row per warp with
 // the fused kernel's rest test and cells_step on T_n (tn, untouched by the
 // stencil) and T_n+1 (tn1).  Rows are independent: list order is irrelevant.
+// Rows [row_lo, nrows) of the state (row_lo % 32 == 0, so the 8 threads that
+// share a hot word are lanes of one warp).
 __global__ void __launch_bounds__(256) rows_scan_kernel(const uint32_t* __restrict__ idle,
                                                         uint32_t* __restrict__ hot,
-                                                        int64_t nrows, uint32_t* __restrict__ list,
+                                                        int64_t row_lo, int64_t nrows,
+                                                        uint32_t* __restrict__ list,
                                                         unsigned int* __restrict__ count) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t r0 = 4 * i;  // rows r0 .. r0+3 (nrows % 4 == 0 is not assumed)
+  const int64_t r0 = row_lo + 4 * i;  // rows r0 .. r0+3 (nrows % 4 == 0 is not assumed)
   unsigned m = 0u;
   uint32_t hw = 0u;
   if (r0 < nrows) {
     hw = hot[r0 >> 5];
     uint32_t v[4];
-    if (r0 + 4 <= nrows && (nrows & 3) == 0 && (reinterpret_cast<uintptr_t>(idle) & 15) == 0) {
-      const uint4 q = reinterpret_cast<const uint4*>(idle)[i];
+    if (r0 + 4 <= nrows && (reinterpret_cast<uintptr_t>(idle + r0) & 15) == 0) {
+      const uint4 q = *reinterpret_cast<const uint4*>(idle + r0);
       v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
     } else {
 #pragma unroll
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(128) rows_kinetics_kernel(const double* __rest
     const int64_t row = list[w];
     const int64_t flat = row * 32 + lane;
     const uint32_t bits = idle[row];
-    const double t0 = tn[flat], t_new = tn1[flat];
+    const double t0 = tn[o.toff + flat], t_new = tn1[o.toff + flat];
     const bool rest = o.rest_ok && ((bits >> lane) & 1u) && t0 < o.kp.t_as_end &&
                       t_new < o.kp.t_as_end;
     cells_step(f, idle, o, lane, true, rest, flat, bits, t0, t_new, gm);
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
         for (int r = 0; r < RY; ++r)
           if (yr[r] < ny)
             cp_async4s(ibase + 4u * (unsigned)(slot * TYT + ty + r * TY),
-                       idle + (((int64_t)zz * plane + (int64_t)yr[r] * nx + (x - lane)) >> 5));
+                       idle + (((int64_t)(zz - o.sz0) * plane + (int64_t)yr[r] * nx + (x - lane)) >> 5));
       }
     }
     cp_async_commit();
@@ -438,7 +445,7 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
           dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
         }
         if (COUPLED)
-          cell_kinetics<COUPLED ? 1 : 0>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
+          cell_kinetics<COUPLED ? 1 : 0>(f, idle, o, lane, in[r], (int64_t)(z - o.sz0) * plane + (int64_t)y * nx + x,
                                  iring[s0 * TYT + ty + r * TY], t0, t_new, gm);
       }
     }
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
         for (int r = 0; r < RY; ++r)
           if (yr[r] < ny)
             cp_async4s(ibase + 4u * (unsigned)(slot * TYT + ty + r * TY),
-                       idle + (((int64_t)zz * plane + (int64_t)yr[r] * nx + x0) >> 5));
+                       idle + (((int64_t)(zz - o.sz0) * plane + (int64_t)yr[r] * nx + x0) >> 5));
       }
       cp_async_commit();
     }
@@ -652,7 +659,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
         if constexpr (CM == 2)
           hr[r] = max((unsigned)__double2hiint(t0), (unsigned)__double2hiint(t_new));
         else if (COUPLED)
-          cell_kinetics<CM>(f, idle, o, lane, true, (int64_t)z * plane + (int64_t)yr[r] * nx + x,
+          cell_kinetics<CM>(f, idle, o, lane, true, (int64_t)(z - o.sz0) * plane + (int64_t)yr[r] * nx + x,
                                  CM == 1 ? iring[s0 * TYT + ty + r * TY] : 0u, t0, t_new, gm);
       }
       if constexpr (CM == 2) {  // the screen of cell_kinetics<2>, both rows at once
@@ -664,7 +671,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
 #pragma unroll
           for (int r = 0; r < RY; ++r)
             if (hr[r] >= thi) {
-              const int64_t row = ((int64_t)z * plane + (int64_t)yr[r] * nx + x) >> 5;
+              const int64_t row = ((int64_t)(z - o.sz0) * plane + (int64_t)yr[r] * nx + x) >> 5;
               atomicOr(o.hot + (row >> 5), 1u << (row & 31));
             }
         }
@@ -699,7 +706,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
           dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
         }
         if (COUPLED)
-          cell_kinetics<CM>(f, idle, o, lane, in[r], (int64_t)z * plane + (int64_t)y * nx + x,
+          cell_kinetics<CM>(f, idle, o, lane, in[r], (int64_t)(z - o.sz0) * plane + (int64_t)y * nx + x,
                                  CM == 1 ? iring[s0 * TYT + ty + r * TY] : 0u, t0, t_new, gm);
       }
     }
@@ -779,8 +786,8 @@ bool launch_built(const double* src, double* dst, const ti64_stencil_args& a,
   return true;
 }
 
-__global__ void idle_bits_init_kernel(ti64_fields f, uint32_t* idle, int64_t n) {
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void idle_bits_init_kernel(ti64_fields f, uint32_t* idle, int64_t lo, int64_t n) {
+  const int64_t w = lo / 32 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w * 32 >= n) return;
   uint32_t b = 0u;
   for (int k = 0; k < 32; ++k) {
@@ -804,51 +811,6 @@ bool use_tma() {
     v = (e && e[0] == '1') ? 0 : 1;
   }
   return v == 1;
-}
-// coupled-step mode: split (default: stencil marking hot rows in a bitmap, then
-// the kinetics of flagged and transformed rows) or fused (TI64_COUPLED_FUSED=1: the kinetics
-// inside the stencil kernel)
-bool coupled_split() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("TI64_COUPLED_FUSED");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-// per-device scratch of the split coupled step: the hot-row bitmap (zeroed at
-// allocation, then word by word by rows_scan_kernel), the row count and the
-// row list; grown on demand, lives for the process like the library's other
-// caches
-struct SplitScratch {
-  uint32_t* hot = nullptr;
-  unsigned int* count = nullptr;
-  uint32_t* list = nullptr;
-  int64_t rows = 0;
-};
-SplitScratch* split_scratch(int64_t nrows) {
-  static std::mutex mu;
-  static SplitScratch sc[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> g(mu);
-  SplitScratch& s = sc[dev & 63];
-  if (s.rows < nrows) {
-    if (s.hot) cudaFree(s.hot);
-    s = SplitScratch{};
-    const int64_t hw = (nrows + 31) / 32 + 4;  // + the count word, 16-B aligned list
-    void* p = nullptr;
-    if (cudaMalloc(&p, (hw + nrows) * sizeof(uint32_t)) != cudaSuccess) return nullptr;
-    if (cudaMemset(p, 0, hw * sizeof(uint32_t)) != cudaSuccess) {
-      cudaFree(p);
-      return nullptr;
-    }
-    s.hot = static_cast<uint32_t*>(p);
-    s.count = reinterpret_cast<unsigned int*>(s.hot + (nrows + 31) / 32);
-    s.list = s.hot + hw;
-    s.rows = nrows;
-  }
-  return &s;
 }
 }  // namespace
 
@@ -906,17 +868,30 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
   return TI64_OK;
 }
 
+// scratch of the split step for a state of n_cells cells: the hot-row bitmap
+// (1 bit per 32-cell row), the row count (+ pad to 16 B) and the row list
+extern "C" int64_t ti64_coupled_scratch_words(int64_t n_cells) {
+  if (n_cells < 0) return TI64_EINVAL;
+  const int64_t nrows = (n_cells + 31) / 32;
+  return (nrows + 31) / 32 + 4 + nrows;
+}
+
 extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti64_fields* f,
-                                     uint32_t* idle_bits_d, const ti64_thermal* tp,
+                                     int64_t state_z0, uint32_t* idle_bits_d,
+                                     uint32_t* scratch_d, const ti64_thermal* tp,
                                      const ti64_stencil_args* a, const ti64_kparams* kp,
                                      const ti64_icfg* cfg, int64_t lanes, int32_t init_bits,
                                      void* stream) {
   if (!tn_d || !tn1_d || !f || !idle_bits_d || !tp || !a || !kp || !cfg || tn_d == tn1_d ||
-      !a->all_built || a->losses_on || a->nx % 32 != 0 || a->z_base != 0 ||
-      a->nz_stored != a->nz || a->z_begin != 0 || a->z_end != a->z_top || a->z_top != a->nz ||
+      !a->all_built || a->losses_on || a->nx % 32 != 0 || a->nx < 1 || a->ny < 1 ||
+      a->z_top != a->nz || a->z_begin < 0 || a->z_end > a->nz || a->z_begin > a->z_end ||
+      a->z_begin < a->z_base || a->z_end > a->z_base + a->nz_stored ||
+      (a->z_begin > 0 && a->z_begin - 1 < a->z_base) ||
+      (a->z_end < a->nz && a->z_end + 1 > a->z_base + a->nz_stored) ||
+      state_z0 < 0 || a->z_begin < state_z0 ||
       !(lanes == 1 || lanes == 2 || lanes == 4 || lanes == 8)) {
-    ti64_set_error("ti64_coupled_step: bad argument (needs a whole all-built grid, no losses, "
-                   "nx % 32 == 0)");
+    ti64_set_error("ti64_coupled_step: bad argument (all-built grid, no losses, nx % 32 == 0, "
+                   "a slab holding the updated planes and their z neighbours)");
     return TI64_EINVAL;
   }
   if (cfg->scheme != TI64_SCHEME_EXPLICIT) {
@@ -928,9 +903,13 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
     return TI64_EINVAL;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t n = a->nx * a->ny * a->nz;
+  const int64_t plane = a->nx * a->ny;
+  const int64_t c_lo = (a->z_begin - state_z0) * plane;  // state cells of the updated planes
+  const int64_t c_hi = (a->z_end - state_z0) * plane;
+  if (c_hi == c_lo) return TI64_OK;
   if (init_bits)
-    idle_bits_init_kernel<<<(unsigned)(((n + 31) / 32 + 255) / 256), 256, 0, st>>>(*f, idle_bits_d, n);
+    idle_bits_init_kernel<<<(unsigned)(((c_hi - c_lo) / 32 + 255) / 256), 256, 0, st>>>(
+        *f, idle_bits_d, c_lo, c_hi);
   StencilConst c;
   c.inv_rch2 = a->dt / (tp->rho_c * a->h * a->h);
   c.inv_rch = a->dt / (tp->rho_c * a->h);
@@ -949,25 +928,29 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   o.L = (int)lanes;
   o.rest_ok = kp->t_as_end <= kp->t_sol && kp->t_as_end <= kp->t_as_start && cfg->stuck_tol < 0.5;
   o.hot = nullptr;
+  o.sz0 = state_z0;
+  o.toff = (state_z0 - a->z_base) * plane;
   const int zchunk = ZCHUNK;
-  if (use_tma() && coupled_split() && o.rest_ok) {  // (no cold rest: every row runs, fused)
-    const int64_t nrows = n / 32;
-    SplitScratch* sc = split_scratch(nrows);
-    if (!sc) {
-      ti64_set_error("ti64_coupled_step: split-step scratch allocation failed");
-      return TI64_ECUDA;
-    }
-    o.hot = sc->hot;
-    if (launch_built<2>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, a->z_top, zchunk, st)) {
+  const int64_t nzu = a->z_end - a->z_begin;
+  // split step: rows are whole (nx % 32 == 0) and the row range starts on a
+  // hot-word boundary (c_lo % 1024 == 0)
+  if (use_tma() && o.rest_ok && scratch_d && c_lo % 1024 == 0) {
+    const int64_t row_lo = c_lo / 32, row_hi = c_hi / 32;
+    const int64_t nrows_state = row_hi;  // bitmap words cover rows [0, row_hi)
+    uint32_t* hot = scratch_d;
+    unsigned int* count = reinterpret_cast<unsigned int*>(scratch_d + (nrows_state + 31) / 32);
+    uint32_t* list = scratch_d + (nrows_state + 31) / 32 + 4;
+    o.hot = hot;
+    if (launch_built<2>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, nzu, zchunk, st)) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaMemsetAsync(sc->count, 0, sizeof(unsigned int), st);
-      const int64_t thr = (nrows + 3) / 4;
-      rows_scan_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(idle_bits_d, sc->hot, nrows,
-                                                                      sc->list, sc->count);
+      cudaMemsetAsync(count, 0, sizeof(unsigned int), st);
+      const int64_t thr = (row_hi - row_lo + 3) / 4;
+      rows_scan_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(idle_bits_d, hot, row_lo,
+                                                                      row_hi, list, count);
       rows_kinetics_kernel<<<(unsigned)(sms * 8), 128, 0, st>>>(tn_d, tn1_d, *f, idle_bits_d, o,
-                                                                sc->list, sc->count);
+                                                                list, count);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         ti64_set_error(std::string("ti64_coupled_step: ") + cudaGetErrorString(e));
@@ -979,9 +962,8 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
     o.hot = nullptr;  // grid TMA cannot map: the fused cp.async kernel below
   }
   dim3 grid((unsigned)(a->nx / TX), (unsigned)((a->ny + TYT - 1) / TYT),
-            (unsigned)((a->z_top + zchunk - 1) / zchunk));
-  if (!use_tma() || !launch_built<1>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, a->z_top, zchunk,
-                                        st))
+            (unsigned)((nzu + zchunk - 1) / zchunk));
+  if (!use_tma() || !launch_built<1>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, nzu, zchunk, st))
     built_pipe_kernel<true><<<grid, dim3(TX, TY), 0, st>>>(tn_d, tn1_d, *a, c, zchunk, *f,
                                                           idle_bits_d, o);
   cudaError_t e = cudaGetLastError();

@@ -217,18 +217,31 @@ def gather_planes(local, z0, z1, zb, nz, world, rank):
 
 
 class SlabCoupledGPU:
-    """Config 3 on this rank's GPU: z-slab (+ halos) of the grid with the
-    kinetics state of the owned cells; K4 and K1 from libti64b200.so, halo
-    planes over NCCL (torch.distributed point-to-point)."""
+    """Config 3 on this rank's GPU: the z-slab (+ 1-plane halos) of the grid
+    and the kinetics state of the owned cells.
+
+    Grids with nx % 32 == 0 run the split coupled step (ti64_coupled_step in
+    slab form: K4 + hot-row bitmap, row scan, kinetics of listed rows) on
+    ping-pong temperature buffers, with the same edge-planes-first halo
+    schedule as SlabCoupledDriver: each step computes the two edge planes,
+    posts their T_{n+1} to the neighbours' halo planes of the next buffer
+    (NCCL point-to-point, ordered after the edge kernels on the stream),
+    computes the interior planes while the transfer runs, and waits only
+    before the buffers swap.  At world size 1 a step is one call.  Other
+    grids take the reference-shaped path (K4 then step_all per step)."""
 
     def __init__(self, nz, ny, nx, h, rank=0, world=1, device=None, t0=353.0,
                  state0=(0.9, 0.0, 0.1)):
         import torch
+        from . import _lib
         from .batch import GlobalFields, _default_device
         dev = device or _default_device()
         self.nz, self.ny, self.nx, self.h = nz, ny, nx, h
+        self.rank, self.world = rank, world
         z0, z1 = slab_range(nz, rank, world)
         zb, ze = max(z0 - 1, 0), min(z1 + 1, nz)
+        self.z0, self.z1, self.zb, self.ze = z0, z1, zb, ze
+        self.split = nx % 32 == 0
         self.t_old = torch.full((ze - zb, ny, nx), float(t0), dtype=torch.float64, device=dev)
         self.t_new = self.t_old.clone()
         plane = ny * nx
@@ -238,11 +251,20 @@ class SlabCoupledGPU:
         self.fields = GlobalFields(full(state0[0]), full(state0[1]), full(state0[2]),
                                    self.t_old.view(-1)[lo:hi], self.t_new.view(-1)[lo:hi],
                                    device=dev)
-        assert self.fields.temperature_old.data_ptr() == self.t_old.view(-1)[lo:].data_ptr()
-        self.driver = SlabCoupledDriver(nz, ny, nx, rank, world, self.t_old, self.t_new,
-                                        self._stencil, self._step, torch_exchange)
         self.step = 0
+        self.device = dev
+        if self.split:
+            self._idle_bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
+            words = _lib.check(_lib.require().ti64_coupled_scratch_words(n),
+                               "ti64_coupled_scratch_words")
+            self._scratch = torch.zeros(words, dtype=torch.int32, device=dev)
+            self._bits_valid = False
+            self._cur, self._nxt = self.t_old, self.t_new
+        else:
+            self.driver = SlabCoupledDriver(nz, ny, nx, rank, world, self.t_old, self.t_new,
+                                            self._stencil, self._step, torch_exchange)
 
+    # --- reference-shaped path (any nx) ---------------------------------
     def _stencil(self, src, dst, args):
         import ctypes as C
         from . import _abi, _lib
@@ -256,17 +278,102 @@ class SlabCoupledGPU:
         from .batch import step_all
         step_all(self.fields, dt, n_lanes=8)
 
-    def run(self, n_steps, dt, beams, source, bottom=353.0):
-        from . import _abi
-        k0 = self.step
+    # --- split coupled step in slab form ----------------------------------
+    def _coupled(self, cur, nxt, z_begin, z_end, dt, beam, source, bottom, consts):
+        import ctypes as C
+        from . import _abi, _lib
+        tp, kpc, cfgc, fs, lanes = consts
+        a = _abi.stencil_args(self.nx, self.ny, self.nz, self.nz, dt, self.h, beam=beam,
+                              source=source, losses=False, bottom=bottom, all_built=True,
+                              slab=(self.zb, self.ze - self.zb, z_begin, z_end))
+        rc = _lib.require().ti64_coupled_step(
+            _lib.ptr(cur), _lib.ptr(nxt), C.byref(fs), self.z0, _lib.ptr(self._idle_bits),
+            _lib.ptr(self._scratch), C.byref(tp), C.byref(a), C.byref(kpc), C.byref(cfgc),
+            int(lanes), 0 if self._bits_valid else 1, _lib.stream_handle())
+        _lib.check(rc, "ti64_coupled_step")
 
-        def args_for(slab, k=None):
-            return _abi.stencil_args(self.nx, self.ny, self.nz, self.nz, dt, self.h,
-                                     beam=beams[self._k], source=source, losses=False,
-                                     bottom=bottom, all_built=True, slab=slab)
+    def _halo_ops(self, buf):
+        """Edge planes of `buf` to the neighbours' halo planes of their `buf`."""
+        lo, hi = self.z0 - self.zb, self.z1 - self.zb
+        ops = []
+        if self.rank > 0:
+            ops.append(("send", buf[lo], self.rank - 1))
+            ops.append(("recv", buf[lo - 1], self.rank - 1))
+        if self.rank < self.world - 1:
+            ops.append(("send", buf[hi - 1], self.rank + 1))
+            ops.append(("recv", buf[hi], self.rank + 1))
+        return ops
+
+    def run(self, n_steps, dt, beams, source, bottom=353.0, kinetics_params=None,
+            integrator_config=None, n_lanes=8):
+        from . import _abi
+        if not self.split:
+            def args_for(slab):
+                return _abi.stencil_args(self.nx, self.ny, self.nz, self.nz, dt, self.h,
+                                         beam=beams[self._k], source=source, losses=False,
+                                         bottom=bottom, all_built=True, slab=slab)
+            for k in range(n_steps):
+                self._k = k
+                self.driver.run_step(dt, args_for)
+                self.step += 1
+            return self
+        self.begin(dt, source, bottom, kinetics_params, integrator_config, n_lanes)
+        if self.world > 1 and self.step == 0:
+            torch_exchange(self._halo_ops(self._cur))  # halos of the initial T
         for k in range(n_steps):
-            self._k = k
-            self.driver.run_step(dt, args_for)
-            self.step += 1
-        del k0
+            if self.world == 1:
+                self.phase_all(beams[k])
+            else:
+                self.phase_edges(beams[k])
+                pending = torch_exchange(self._halo_ops(self._nxt), wait=False)
+                self.phase_interior(beams[k])
+                pending.wait()
+            self.finish_step()
+        return self.end(n_steps)
+
+    # phases of one split step (exposed so a test can interleave several
+    # slabs on one device, exchanging halos with plain copies)
+    def begin(self, dt, source, bottom=353.0, kinetics_params=None, integrator_config=None,
+              n_lanes=8):
+        from . import _abi
+        from .integrator import IntegratorConfig
+        from .kinetics import DEFAULT_PARAMS
+        from .thermal import DEFAULT_THERMAL
+        kp = kinetics_params or DEFAULT_PARAMS
+        cfg = integrator_config or IntegratorConfig(scheme="explicit")
+        self._run = (dt, source, bottom,
+                     (_abi.thermal_from(DEFAULT_THERMAL.kernel_tuple()),
+                      _abi.kparams_from(kp.kernel_tuple()), _abi.icfg_from(cfg.kernel_tuple()),
+                      self.fields.cstruct(), n_lanes))
+
+    def _do(self, z_begin, z_end, beam):
+        dt, source, bottom, consts = self._run
+        self._coupled(self._cur, self._nxt, z_begin, z_end, dt, beam, source, bottom, consts)
+
+    def phase_all(self, beam):
+        self._do(self.z0, self.z1, beam)
+
+    def phase_edges(self, beam):
+        for z in sorted({self.z0, self.z1 - 1}):
+            self._do(z, z + 1, beam)
+
+    def phase_interior(self, beam):
+        if self.z1 - self.z0 > 2:
+            self._do(self.z0 + 1, self.z1 - 1, beam)
+
+    def finish_step(self):
+        self._bits_valid = True
+        self._cur, self._nxt = self._nxt, self._cur
+        self.step += 1
+
+    def end(self, n_steps):
+        # the reference ends a step with temperature_old == temperature_new
+        other = self.t_new if self._cur is self.t_old else self.t_old
+        other.copy_(self._cur)
+        self.fields.traffic_bytes += 72 * self.fields.n_points * n_steps
+        self.fields.steps_taken += n_steps
         return self
+
+    def temperature(self):
+        """The owned planes of the current T (a view)."""
+        return self._cur[self.z0 - self.zb:self.z1 - self.zb]

@@ -269,16 +269,18 @@ class CoupledDomain:
         self.step = 0
         self._idle_bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
         self._bits_valid = False
+        self._split_scratch = None  # the split step's row bitmap / list (allocated on use)
         del np
 
     def run(self, n_steps, dt, beams, source, kinetics_params=None, integrator_config=None,
-            thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8, fused=None):
+            thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8, fused=None,
+            split=True):
         """n_steps coupled steps; beams[k] = (x, y, power, on) of step k.
 
         fused=True (default when nx % 32 == 0 and no losses) runs the device
-        coupled step with ping-pong temperatures (bit-identical results): the
-        stencil marking hot rows, then the kinetics of hot and transformed rows
-        only (TI64_COUPLED_FUSED=1: one K4+kinetics kernel);
+        coupled step with ping-pong temperatures (bit-identical results): with
+        split=True the stencil marks hot rows, then the kinetics of hot and
+        transformed rows run (split=False: one K4+kinetics kernel);
         fused=False issues step_thermal + step_all per step like the reference."""
         from .batch import step_all
         from .integrator import IntegratorConfig
@@ -297,9 +299,10 @@ class CoupledDomain:
                 self.step += 1
             return self
         return self._run_fused(n_steps, dt, beams, source, kp, cfg, thermal_params, bottom,
-                               n_lanes)
+                               n_lanes, split)
 
-    def _run_fused(self, n_steps, dt, beams, source, kp, cfg, thermal_params, bottom, n_lanes):
+    def _run_fused(self, n_steps, dt, beams, source, kp, cfg, thermal_params, bottom, n_lanes,
+                   split=True):
         import ctypes as C
         from . import _abi, _lib
         lib = _lib.require()
@@ -312,14 +315,21 @@ class CoupledDomain:
         cfgc = _abi.icfg_from(cfg.kernel_tuple())
         fs = self.fields.cstruct()
         st = _lib.stream_handle()
+        if split and self._split_scratch is None:
+            import torch
+            words = _lib.check(lib.ti64_coupled_scratch_words(nx * ny * nz),
+                               "ti64_coupled_scratch_words")
+            self._split_scratch = torch.zeros(words, dtype=torch.int32,
+                                              device=self.fields.device)
         cur, nxt = self.fields.temperature_old, self.fields.temperature_new
         for k in range(n_steps):
             a = _abi.stencil_args(nx, ny, nz, nz, dt, self.field.h, beam=beams[k],
                                   source=source, losses=False, bottom=bottom, all_built=True)
-            rc = lib.ti64_coupled_step(_lib.ptr(cur), _lib.ptr(nxt), C.byref(fs),
-                                       _lib.ptr(self._idle_bits), C.byref(tp), C.byref(a),
-                                       C.byref(kpc), C.byref(cfgc), int(n_lanes),
-                                       0 if self._bits_valid else 1, st)
+            rc = lib.ti64_coupled_step(_lib.ptr(cur), _lib.ptr(nxt), C.byref(fs), 0,
+                                       _lib.ptr(self._idle_bits),
+                                       _lib.ptr(self._split_scratch) if split else None,
+                                       C.byref(tp), C.byref(a), C.byref(kpc), C.byref(cfgc),
+                                       int(n_lanes), 0 if self._bits_valid else 1, st)
             _lib.check(rc, "ti64_coupled_step")
             self._bits_valid = True
             cur, nxt = nxt, cur

@@ -216,7 +216,7 @@ def test_cp_async_pipeline_equals_tma(env, tmp_path):
 
 def test_split_coupled_step_equals_fused(env, tmp_path):
     """The split coupled step (default: stencil + hot-row bitmap, row scan,
-    one warp per listed row) and the fused kernel (TI64_COUPLED_FUSED=1) give
+    one warp per listed row) and the fused kernel (split=False) give
     the same bits: temperatures, phase fractions, seed arrays and counters
     after 300 steps of a moving source (hot rows, a transformed trail)."""
     import os
@@ -225,13 +225,84 @@ def test_split_coupled_step_equals_fused(env, tmp_path):
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     outs = []
-    for flag in ("0", "1"):
-        out = tmp_path / f"mode_{flag}.npz"
-        e = dict(os.environ, TI64_COUPLED_FUSED=flag)
-        subprocess.run([sys.executable, str(root / "tools" / "stencil_ab.py"), str(out)],
-                       env=e, check=True, cwd=root)
+    for mode in ("split", "fused"):
+        out = tmp_path / f"mode_{mode}.npz"
+        subprocess.run([sys.executable, str(root / "tools" / "stencil_ab.py"), str(out), mode],
+                       env=dict(os.environ), check=True, cwd=root)
         outs.append(np.load(out))
     xs = outs[0]["x_alpha_s"]
     assert np.count_nonzero(xs != 0.9) > 0  # the trail exists: split rows were run
     for k in outs[0].files:
         assert_bitwise(outs[0][k], outs[1][k], f"split vs fused {k}")
+
+
+def _config3_like(th, nz, ny, nx, h, dt, nsteps):
+    from paper_2402_17580_b200 import scanpath
+    src = th.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=h)
+    segs = scanpath.serpentine((0.2e-3, 0.2e-3, 1.0e-3, 0.6e-3), 80e-6, 1.0, 87.5)
+    return src, scanpath.beam_schedule(segs, nsteps, dt)
+
+
+def test_slab_split_single_rank_equals_coupled(env):
+    """The slab-form split coupled step at world size 1 (one call per step)
+    equals the whole-grid coupled domain, every array bit for bit."""
+    th = env["th"]
+    from paper_2402_17580_b200.distributed import SlabCoupledGPU
+    nz, ny, nx, h, dt, nsteps = 16, 40, 64, 20e-6, 1e-6, 300
+    src, beams = _config3_like(th, nz, ny, nx, h, dt, nsteps)
+    a = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=h).run(nsteps, dt, beams, src)
+    b = SlabCoupledGPU(nz, ny, nx, h)
+    assert b.split
+    b.run(nsteps // 3, dt, beams, src)
+    b.run(nsteps - nsteps // 3, dt, beams[nsteps // 3:], src)
+    ha, hb = a.fields.to_host(), b.fields.to_host()
+    assert ha["temperature_old"].max() > 1500.0
+    assert np.count_nonzero(ha["x_alpha_s"] != 0.9) > 0
+    for k in ha:
+        assert_bitwise(ha[k], hb[k], f"slab split {k}")
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_slab_split_emulated_ranks_equal_whole_grid(env, world):
+    """The multi-GPU schedule of SlabCoupledGPU (edge planes, halo exchange
+    of the new edge planes into the neighbours' next buffers, interior
+    planes, swap) with `world` slabs interleaved on one device and the
+    exchange done by copies, against the whole grid: every owned cell's
+    temperature and kinetics state bit for bit."""
+    import torch
+    th = env["th"]
+    from paper_2402_17580_b200.distributed import SlabCoupledGPU
+    nz, ny, nx, h, dt, nsteps = 15, 40, 64, 20e-6, 1e-6, 240
+    src, beams = _config3_like(th, nz, ny, nx, h, dt, nsteps)
+    a = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=h).run(nsteps, dt, beams, src)
+    ranks = [SlabCoupledGPU(nz, ny, nx, h, rank=r, world=world) for r in range(world)]
+
+    def exchange():
+        for r, s in enumerate(ranks):  # edge planes -> neighbours' halo planes
+            lo, hi = s.z0 - s.zb, s.z1 - s.zb
+            if r > 0:
+                nb = ranks[r - 1]
+                nb._nxt[nb.z1 - nb.zb].copy_(s._nxt[lo])
+            if r < world - 1:
+                nb = ranks[r + 1]
+                nb._nxt[nb.z0 - 1 - nb.zb].copy_(s._nxt[hi - 1])
+
+    for s in ranks:
+        s.begin(dt, src)
+    for k in range(nsteps):
+        for s in ranks:
+            s.phase_edges(beams[k])
+        exchange()
+        for s in ranks:
+            s.phase_interior(beams[k])
+        for s in ranks:
+            s.finish_step()
+    for s in ranks:
+        s.end(nsteps)
+    T = torch.cat([s.temperature() for s in ranks], 0).cpu().numpy().ravel()
+    ha = a.fields.to_host()
+    assert_bitwise(T, ha["temperature_old"], f"world {world} T")
+    for k in ("x_alpha_s", "x_alpha_m", "x_beta", "seed_active", "seed_tracked",
+              "seed_direction"):
+        got = np.concatenate([s.fields.host(k) for s in ranks])
+        assert_bitwise(got, ha[k], f"world {world} {k}")

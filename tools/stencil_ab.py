@@ -1,6 +1,6 @@
 """Helper for tests/test_gpu_stencil.py: run K4 and the fused coupled step on
 an odd-sized grid and save the results (the pipeline is chosen by TI64_NO_TMA,
-the coupled-step mode by TI64_COUPLED_FUSED)."""
+the coupled-step mode by the second argument: split (default) or fused)."""
 import sys
 from pathlib import Path
 
@@ -15,7 +15,8 @@ src = th.HeatSource(w_eff=87.5, radius=50e-6, h_powder=h)
 segs = scanpath.serpentine((0.2e-3, 0.2e-3, 1.0e-3, 0.6e-3), 80e-6, 1.0, 87.5)
 beams = scanpath.beam_schedule(segs, 300, dt)
 a = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=h)
-a.run(300, dt, beams, src, fused=True)
+split = len(sys.argv) < 3 or sys.argv[2] != "fused"
+a.run(300, dt, beams, src, fused=True, split=split)
 b = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=h)
 b.field.temperature_old.copy_(a.field.temperature_old)
 for k in range(5):
