@@ -87,7 +87,8 @@ class StencilArgs(C.Structure):
                 ("bc_bottom_on", C.c_int32), ("all_built", C.c_int32),
                 ("src_peak", C.c_double), ("src_r2inv", C.c_double),
                 ("bc_bottom", C.c_double), ("z_base", C.c_int64),
-                ("nz_stored", C.c_int64), ("z_begin", C.c_int64), ("z_end", C.c_int64)]
+                ("nz_stored", C.c_int64), ("z_begin", C.c_int64), ("z_end", C.c_int64),
+                ("beam_tab_d", C.c_void_p), ("step_d", C.c_void_p)]
 
 
 def stencil_args(nx, ny, nz, z_top, dt, h, beam=None, source=None, losses=False,

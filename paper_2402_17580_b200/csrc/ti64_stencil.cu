@@ -47,16 +47,39 @@ struct StencilConst {
 
 __device__ __forceinline__ double clip01(double g) { return g < 0.0 ? 0.0 : (g > 1.0 ? 1.0 : g); }
 
+// The beam of this step: from the launch arguments, or (graph replay of a
+// step loop) row *step_d of a device table of (x, y, src_peak, on) rows
+struct SrcRow {
+  int on;
+  double bx, by, coef;  // coef = inv_rc * src_peak (association of thermal.py:261)
+};
+
+__device__ __forceinline__ SrcRow source_row(const ti64_stencil_args& a, const StencilConst& c) {
+  SrcRow r;
+  if (a.beam_tab_d) {
+    const double* b = a.beam_tab_d + 4 * (*a.step_d);
+    r.bx = b[0];
+    r.by = b[1];
+    r.coef = __dmul_rn(c.inv_rc, b[2]);
+    r.on = b[3] != 0.0;
+  } else {
+    r.bx = a.beam_x;
+    r.by = a.beam_y;
+    r.coef = c.src_coef;
+    r.on = a.source_on != 0;
+  }
+  return r;
+}
+
 // top-layer Gaussian source term (thermal.py:255-261)
 __device__ __forceinline__ double add_source(double t_new, int64_t x, int64_t y,
-                                             const ti64_stencil_args& a,
-                                             const StencilConst& c) {
+                                             const ti64_stencil_args& a, const SrcRow& sr) {
   const double xc = __dmul_rn(__dadd_rn((double)x, 0.5), a.h);
   const double yc = __dmul_rn(__dadd_rn((double)y, 0.5), a.h);
-  const double dx = __dsub_rn(xc, a.beam_x), dy = __dsub_rn(yc, a.beam_y);
+  const double dx = __dsub_rn(xc, sr.bx), dy = __dsub_rn(yc, sr.by);
   const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
   const double arg = __dmul_rn(__dmul_rn(-2.0, r2), a.src_r2inv);
-  if (arg > -40.0) t_new = __dadd_rn(t_new, __dmul_rn(c.src_coef, fast_exp(arg)));
+  if (arg > -40.0) t_new = __dadd_rn(t_new, __dmul_rn(sr.coef, fast_exp(arg)));
   return t_new;
 }
 
@@ -103,7 +126,8 @@ __global__ void __launch_bounds__(256) stencil_general_kernel(const double* __re
     flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(t1, t0)));
   }
   double t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
-  if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
+  const SrcRow sr = source_row(a, c);
+  if (sr.on && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, sr);
   if (a.losses_on != 0) {
     const bool exposed = z == nz - 1 || state[idx + plane] == STATE_INACTIVE;
     if (exposed) {
@@ -368,6 +392,7 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
   const int z1 = min(z0 + zchunk, (int)a.z_end);
   if (z0 >= z1) return;
   const int64_t plane = (int64_t)nx * ny;
+  const SrcRow sr = source_row(a, c);
   const int zlo = max(0, (int)a.z_base), zhi = min(nz, (int)(a.z_base + a.nz_stored));
   const unsigned rbase = (unsigned)__cvta_generic_to_shared(ring);
   const unsigned ibase = (unsigned)__cvta_generic_to_shared(iring);
@@ -440,7 +465,7 @@ __global__ void __launch_bounds__(TX* TY) built_pipe_kernel(
           if (z + 1 < nz)
             flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sp1 * SLOT + cidx[r]], t0)));
           t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
-          if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
+          if (sr.on && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, sr);
           if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
           dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
         }
@@ -567,6 +592,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
   const int z1 = min(z0 + zchunk, (int)a.z_end);
   if (z0 >= z1) return;
   const int64_t plane = (int64_t)nx * ny;
+  const SrcRow sr = source_row(a, c);
   const int zlo = max(0, (int)a.z_base), zhi = min(nz, (int)(a.z_base + a.nz_stored));
   const int zmax = min(zhi, z1 + 1);
   // the descriptor address is taken here, in the kernel body: a lambda that
@@ -639,7 +665,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
       cp_async_wait<PD>();
       __syncthreads();
     }
-    if (xy_interior && z > 0 && z + 1 < nz && !(a.source_on != 0 && z == a.z_top - 1)) {
+    if (xy_interior && z > 0 && z + 1 < nz && !(sr.on && z == a.z_top - 1)) {
       // interior plane of an interior tile: all six faces present, no source
       // or boundary value; same face order and association as below
       double* dz = dcol + (int64_t)z * plane;
@@ -701,7 +727,7 @@ __global__ void __launch_bounds__(TX* TY, CM == 1 ? TMA_MINB_C : TMA_MINB) built
           if (z + 1 < nz)
             flux = __dadd_rn(flux, __dmul_rn(kf, __dsub_rn(ring[sp1 * SLOTD + cidx[r]], t0)));
           t_new = __dadd_rn(t0, __dmul_rn(c.inv_rch2, flux));
-          if (a.source_on != 0 && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, c);
+          if (sr.on && z == a.z_top - 1) t_new = add_source(t_new, x, y, a, sr);
           if (a.bc_bottom_on != 0 && z == 0) t_new = a.bc_bottom;  // thermal.py:274-278
           dcol[(int64_t)z * plane + (int64_t)y * nx] = t_new;
         }
@@ -865,6 +891,24 @@ extern "C" int64_t ti64_stencil_step(const double* src_d, double* dst_d, double*
     return TI64_ECUDA;
   }
   ti64_set_error("");
+  return TI64_OK;
+}
+
+namespace {
+__global__ void step_counter_kernel(int64_t* step_d, int64_t k) { *step_d += k; }
+}  // namespace
+
+extern "C" int64_t ti64_step_counter_add(int64_t* step_d, int64_t k, void* stream) {
+  if (!step_d) {
+    ti64_set_error("ti64_step_counter_add: bad argument");
+    return TI64_EINVAL;
+  }
+  step_counter_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(step_d, k);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ti64_set_error(std::string("ti64_step_counter_add: ") + cudaGetErrorString(e));
+    return TI64_ECUDA;
+  }
   return TI64_OK;
 }
 

@@ -242,6 +242,18 @@ def step_thermal(field, dt, params=DEFAULT_THERMAL, source=None, beam=None, loss
     return field
 
 
+def beam_rows(beams, source):
+    """(n, 4) float64 device-table rows (x, y, src_peak, on) of a beam
+    schedule, with the arithmetic of _abi.stencil_args (thermal.py:255-261)."""
+    import numpy as np
+    out = np.zeros((len(beams), 4))
+    for k, b in enumerate(beams):
+        if b[3]:
+            out[k] = (b[0], b[1],
+                      2.0 * b[2] / (math.pi * source.radius ** 2 * source.h_powder), 1.0)
+    return out
+
+
 class CoupledDomain:
     """Config 3: a fully built (nz, ny, nx) block, kinetics state at every
     cell, driven per step exactly as run_build's `couple` does
@@ -274,14 +286,17 @@ class CoupledDomain:
 
     def run(self, n_steps, dt, beams, source, kinetics_params=None, integrator_config=None,
             thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8, fused=None,
-            split=True):
+            split=True, graph=False):
         """n_steps coupled steps; beams[k] = (x, y, power, on) of step k.
 
         fused=True (default when nx % 32 == 0 and no losses) runs the device
         coupled step with ping-pong temperatures (bit-identical results): with
         split=True the stencil marks hot rows, then the kinetics of hot and
         transformed rows run (split=False: one K4+kinetics kernel);
-        fused=False issues step_thermal + step_all per step like the reference."""
+        fused=False issues step_thermal + step_all per step like the reference.
+        graph=True (fused path) reads each step's beam from a device table and
+        replays a captured two-step CUDA graph (one host call per two steps;
+        same results)."""
         from .batch import step_all
         from .integrator import IntegratorConfig
         from .kinetics import DEFAULT_PARAMS
@@ -299,10 +314,10 @@ class CoupledDomain:
                 self.step += 1
             return self
         return self._run_fused(n_steps, dt, beams, source, kp, cfg, thermal_params, bottom,
-                               n_lanes, split)
+                               n_lanes, split, graph)
 
     def _run_fused(self, n_steps, dt, beams, source, kp, cfg, thermal_params, bottom, n_lanes,
-                   split=True):
+                   split=True, graph=False):
         import ctypes as C
         from . import _abi, _lib
         lib = _lib.require()
@@ -322,18 +337,53 @@ class CoupledDomain:
             self._split_scratch = torch.zeros(words, dtype=torch.int32,
                                               device=self.fields.device)
         cur, nxt = self.fields.temperature_old, self.fields.temperature_new
-        for k in range(n_steps):
-            a = _abi.stencil_args(nx, ny, nz, nz, dt, self.field.h, beam=beams[k],
-                                  source=source, losses=False, bottom=bottom, all_built=True)
-            rc = lib.ti64_coupled_step(_lib.ptr(cur), _lib.ptr(nxt), C.byref(fs), 0,
-                                       _lib.ptr(self._idle_bits),
-                                       _lib.ptr(self._split_scratch) if split else None,
-                                       C.byref(tp), C.byref(a), C.byref(kpc), C.byref(cfgc),
-                                       int(n_lanes), 0 if self._bits_valid else 1, st)
+        scr = _lib.ptr(self._split_scratch) if split else None
+
+        def call(src, dst, a, stream):
+            rc = lib.ti64_coupled_step(_lib.ptr(src), _lib.ptr(dst), C.byref(fs), 0,
+                                       _lib.ptr(self._idle_bits), scr, C.byref(tp), C.byref(a),
+                                       C.byref(kpc), C.byref(cfgc), int(n_lanes),
+                                       0 if self._bits_valid else 1, stream)
             _lib.check(rc, "ti64_coupled_step")
             self._bits_valid = True
+
+        if graph and n_steps >= 3:
+            import torch
+            dev = self.fields.device
+            tab = torch.from_numpy(beam_rows(beams[:n_steps], source)).to(dev)
+            ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+            a = _abi.stencil_args(nx, ny, nz, nz, dt, self.field.h, beam=None, source=None,
+                                  losses=False, bottom=bottom, all_built=True)
+            a.src_r2inv = 1.0 / source.radius ** 2
+            a.beam_tab_d, a.step_d = tab.data_ptr(), ctr.data_ptr()
+
+            def step(src, dst, stream):
+                call(src, dst, a, stream)
+                _lib.check(lib.ti64_step_counter_add(_lib.ptr(ctr), 1, stream),
+                           "ti64_step_counter_add")
+
+            step(cur, nxt, st)  # eager first step (initialises the idle bits)
             cur, nxt = nxt, cur
-            self.step += 1
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                cs = _lib.stream_handle()
+                step(cur, nxt, cs)
+                step(nxt, cur, cs)
+            for _ in range((n_steps - 1) // 2):
+                g.replay()
+            if (n_steps - 1) % 2:
+                step(cur, nxt, st)
+                cur, nxt = nxt, cur
+            torch.cuda.current_stream().synchronize()  # keep tab / ctr alive to the end
+            del g
+            self.step += n_steps
+        else:
+            for k in range(n_steps):
+                a = _abi.stencil_args(nx, ny, nz, nz, dt, self.field.h, beam=beams[k],
+                                      source=source, losses=False, bottom=bottom, all_built=True)
+                call(cur, nxt, a, st)
+                cur, nxt = nxt, cur
+                self.step += 1
         # the reference ends a step with temperature_old == temperature_new
         if cur is self.fields.temperature_new:
             self.fields.temperature_old.copy_(cur)
