@@ -73,8 +73,10 @@ F_BASE, F_FORM, F_GA, F_GROW, F_AM, F_DIS, F_TAIL = 48, 22, 46, 49, 49, 98, 18
 # executed view and DRAM traffic of the headline launch, from the committed
 # ncu capture of the bench workload (profiles/README.md, round 2)
 K2_PROFILE = {
-    "file": "profiles/r02_advance_cfg4_window.txt",
-    "dram_bytes_per_launch": None, "fp64_pipe_active": None, "issue_active": None,
+    "file": "profiles/r02a_advance_cfg4_window.txt (ncu --set full of the first timed window "
+            "launch, 2^27 points, steps 20200-20400)",
+    "dram_bytes_per_launch": 38_838_518_000 + 79_459_955_000,  # read + write
+    "fp64_pipe_active": 0.5255, "issue_active": 0.8029,
 }
 
 
@@ -418,6 +420,12 @@ def run_reference_arm(args):
                                  f, gen, pts, t_start, c["window"], args.steps, 1e30, threads)
         desc = (f"oracle/ti64_oracle.c step_all (port; the reference could not be imported: "
                 f"{why}), lanes=8, OpenMP {threads} threads on {cpu_model()}")
+    cfg3 = None
+    if mods is not None and not args.no_config3:
+        try:
+            cfg3 = reference_config3_step(mods, threads)
+        except Exception as e:  # keep the headline line even if this extra fails
+            cfg3 = {"error": f"{type(e).__name__}: {e}"}
     upd = len(pts) * c["window"] * wins
     value = upd / secs
     sample = (f"every {c['stride']}th point of the 2^27 ({len(pts)} points) x {wins} window(s) "
@@ -436,9 +444,58 @@ def run_reference_arm(args):
                                 "timed_seconds": secs,
                                 "ms_per_step_note": "one step = one window of the bounded "
                                                     "sample (not of all 2^27 points)",
-                                "reference_equals_oracle_bitwise": check}}
+                                "reference_equals_oracle_bitwise": check,
+                                "config3_full_grid_step": cfg3}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def reference_config3_step(mods, threads):
+    """BASELINE.md §3 for config 3: one full-grid 512x512x256 coupled step of
+    the reference on the host — thermal.step_thermal(field, 1e-6,
+    losses=False, bottom_dirichlet=353) (serial numba _stencil_step) then
+    step_all (n_lanes=8, all threads) on the aliased temperature buffers, as
+    run_build's couple does (thermal.py:541-555); JIT excluded."""
+    import importlib
+    rbatch, rinteg, rkin = mods
+    rth = importlib.import_module("ti64micro.thermal")
+    nz, ny, nx, h = 256, 512, 512, 20e-6
+    src = rth.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=h)
+    beam = (5e-3, 5e-3, 0.35 * 250.0, True)
+    rcfg = rinteg.IntegratorConfig(scheme="explicit")
+
+    def domain(nz_, ny_, nx_):
+        n = nz_ * ny_ * nx_
+        t_old, t_new = np.full(n, 353.0), np.full(n, 353.0)
+        f = rbatch.GlobalFields(np.full(n, 0.9), np.zeros(n), np.full(n, 0.1), t_old, t_new)
+        field = rth.ThermalField(f.temperature_old.reshape(nz_, ny_, nx_),
+                                 f.temperature_new.reshape(nz_, ny_, nx_),
+                                 np.ones((nz_, ny_, nx_)),
+                                 np.full((nz_, ny_, nx_), 2, np.uint8), h, nz_)
+        return f, field
+
+    def step(f, field):
+        rth.step_thermal(field, 1e-6, rth.DEFAULT_THERMAL, src, beam, losses=False,
+                         bottom_dirichlet=353.0)
+        rbatch.step_all(f, 1e-6, rkin.DEFAULT_PARAMS, rcfg, n_lanes=8, threads=threads)
+
+    c0 = time.perf_counter()
+    step(*domain(4, 8, 8))  # JIT warm-up
+    jit = time.perf_counter() - c0
+    f, field = domain(nz, ny, nx)
+    c0 = time.perf_counter()
+    rth.step_thermal(field, 1e-6, rth.DEFAULT_THERMAL, src, beam, losses=False,
+                     bottom_dirichlet=353.0)
+    t_st = time.perf_counter() - c0
+    c0 = time.perf_counter()
+    rbatch.step_all(f, 1e-6, rkin.DEFAULT_PARAMS, rcfg, n_lanes=8, threads=threads)
+    t_sa = time.perf_counter() - c0
+    n = nz * ny * nx
+    return {"cell_steps_per_s": n / (t_st + t_sa), "seconds": t_st + t_sa,
+            "step_thermal_seconds": t_st, "step_all_seconds": t_sa, "jit_seconds": jit,
+            "what": "one full-grid 512x512x256 step: step_thermal (serial numba _stencil_step, "
+                    "losses off, Dirichlet 353 K) + step_all (n_lanes=8, threads="
+                    f"{threads}) of the unmodified reference"}
 
 
 # ---------------------------------------------------------------------------
@@ -531,7 +588,8 @@ def measure_ode(torch, pkg, cfg_id, K, W, rank, world, dev, dd, *, counted=True,
     t_first = s
     start_copy = f.copy() if (counted or cpu or e2e) else None
     hist = torch.zeros((3, 256), dtype=torch.int64, device=dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K)]  # window starts
+    ev_w = [torch.cuda.Event(enable_timing=True) for _ in range(K)]  # window ends
     ev_end = torch.cuda.Event(enable_timing=True)
     launches = 0
     sums = None
@@ -547,10 +605,10 @@ def measure_ode(torch, pkg, cfg_id, K, W, rank, world, dev, dd, *, counted=True,
         ev[k].record(stream)
         r = pkg.advance(f, win, src, step0=s, point_offset=lo, snapshot_every=win,
                         scratch=scratch)
+        ev_w[k].record(stream)
         launches += r.launches
         sums = r.sums
         s += win
-    ev[K].record(stream)
     # end of the job's timed part: histogram + cross-rank reduction
     hist.zero_()
     pkg.histogram(f, 256, out=hist)
@@ -561,10 +619,11 @@ def measure_ode(torch, pkg, cfg_id, K, W, rank, world, dev, dd, *, counted=True,
     dd.barrier()
     if clocks is not None:
         clocks.__exit__(None, None, None)
-    t_windows = [ev[k].elapsed_time(ev[k + 1]) * 1e-3 for k in range(K)]
-    # restart mode restores the state between windows (untimed): the region
-    # is the sum of the windows plus the final reduction
-    t_region = sum(t_windows) + ev[K].elapsed_time(ev_end) * 1e-3
+    t_windows = [ev[k].elapsed_time(ev_w[k]) * 1e-3 for k in range(K)]
+    # the region is the sum of the windows plus the final reduction (restart
+    # mode restores the state between windows, untimed; otherwise the
+    # windows are back to back)
+    t_region = sum(t_windows) + ev_w[K - 1].elapsed_time(ev_end) * 1e-3
     t_max = dd.max(t_region)
     out = {"n_local": n, "lo": lo, "t_region": t_region, "t_max": t_max,
            "t_windows": t_windows, "launches": launches, "prep_s": prep_s,
@@ -730,16 +789,16 @@ def measure_extra(torch, pkg, dev, dd, peak_tf, args):
     out["config4_whole_job_2^21_shard"] = {"point_updates_per_s": nsh * CONFIGS[4]["job"] / t,
                                            "seconds": t}
     del f4, scr
-    # config 3: K4 and the split coupled step
+    # config 3: K4, then the whole 20 000-step coupled job (split step)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     nz, ny, nx = 256, 512, 512
     n = nz * ny * nx
-    dom = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=20e-6, device=dev)
+    job3 = 20000
     srcb = th.HeatSource(w_eff=0.35 * 250.0, radius=50e-6, h_powder=20e-6)
     segs = scanpath.serpentine((1e-3, 1e-3, 9.24e-3, 9.24e-3), 80e-6, 1.0, 0.35 * 250.0)
-    beams = scanpath.beam_schedule(segs, 400, 1e-6)
-    dom.run(100, 1e-6, beams, srcb, fused=True)
-    k = [100]
+    beams = scanpath.beam_schedule(segs, job3, 1e-6)
+    dom = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=20e-6, device=dev)
+    k = [0]
 
     def timed(fn, reps):
         ts = []
@@ -762,15 +821,55 @@ def measure_extra(torch, pkg, dev, dd, peak_tf, args):
         "frac_of_measured_hbm": 16 * n / t / 1e9 / hbm,
         "bytes_model": "16 B/cell (8 read T_n + 8 write T_n+1)", "pipeline": "TMA + mbarrier ring",
         "timing": "10 consecutive steps per event pair (inputs 1 GiB > L2)"}
-
-    def coupled():
-        dom.run(10, 1e-6, beams[k[0]:], srcb, fused=True)
-        k[0] += 10
-    t = timed(coupled, 5) / 10
-    out["config3_coupled_step"] = {"cells": n, "ms_per_step": t * 1e3, "cell_steps_per_s": n / t,
-                                   "path": "split: K4 + hot-row bitmap, row scan, kinetics of "
-                                           "listed rows (early in the job)"}
-    del dom, flush
+    del dom
+    dom = th.CoupledDomain(nx=nx, ny=ny, nz=nz, h=20e-6, device=dev)
+    dom.run(1, 1e-6, beams, srcb)  # idle bits, scratch
+    chunk = 5000
+    ts = []
+    s3 = 1
+    while s3 < job3:
+        m = min(chunk, job3 - s3)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dom.run(m, 1e-6, beams[s3:], srcb)
+        b.record()
+        b.synchronize()
+        ts.append((m, a.elapsed_time(b) * 1e-3))
+        s3 += m
+    tot = sum(x for _, x in ts)
+    h3 = dom.fields.to_host()
+    cpu3 = None
+    if not args.no_cpu_baseline:  # one full-grid step on the host (port)
+        from oracle import oracle as orc
+        from paper_2402_17580_b200 import _abi
+        hf = orc.HostFields(h3["x_alpha_s"], h3["x_alpha_m"], h3["x_beta"],
+                            h3["temperature_old"], h3["temperature_new"], h3["seed_tracked"],
+                            h3["seed_active"], h3["seed_direction"])
+        ones, built = np.ones((nz, ny, nx)), np.full((nz, ny, nx), 2, np.uint8)
+        a3 = _abi.stencil_args(nx, ny, nz, nz, 1e-6, 20e-6, beam=beams[-1], source=srcb,
+                               losses=False, bottom=353.0, all_built=True)
+        from paper_2402_17580_b200.kinetics import DEFAULT_PARAMS
+        from paper_2402_17580_b200.integrator import IntegratorConfig
+        c0 = time.perf_counter()
+        orc.stencil_step(hf.temperature_old.reshape(nz, ny, nx),
+                         hf.temperature_new.reshape(nz, ny, nx), ones, built,
+                         th.DEFAULT_THERMAL.kernel_tuple(), a3)
+        orc.step_all(hf, 1e-6, DEFAULT_PARAMS.kernel_tuple(), IntegratorConfig().kernel_tuple(),
+                     n_lanes=8, threads=cpu_threads())
+        t_cpu = time.perf_counter() - c0
+        cpu3 = {"value": n / t_cpu, "unit": "cell-steps/s", "cores": cpu_threads(),
+                "kind": "port", "sample": "one full-grid 512x512x256 step at the job's end: "
+                "oracle stencil_step (OpenMP over planes) + step_all (lanes=8)",
+                "seconds": t_cpu}
+    out["config3_whole_job"] = {
+        "cells": n, "steps": job3, "seconds": tot, "ms_per_step": 1e3 * tot / (job3 - 1),
+        "cell_steps_per_s": n * (job3 - 1) / tot,
+        "ms_per_step_by_chunk": [1e3 * x / m for m, x in ts],
+        "T_max_end": float(h3["temperature_old"].max()),
+        "transformed_cells_end": int(np.count_nonzero(h3["x_alpha_s"] != 0.9)),
+        "path": "split coupled step: K4 + hot-row bitmap, row scan, kinetics of listed rows",
+        "cpu_baseline": cpu3}
+    del dom, flush, h3
     # K1 (one step_all) at 2^26 cold points: the HBM-bound per-step kernel
     n1 = 1 << 26
     f1 = pkg.GlobalFields.allocate(n1, temperature=300.0, device=dev)
@@ -838,6 +937,9 @@ def run_b200(args):
                    "kernel": "advance_kernel<PULSE_SWEEP> (K2), one launch per window",
                    "traffic": K2_PROFILE["dram_bytes_per_launch"],
                    "traffic_source": K2_PROFILE["file"],
+                   "traffic_note": "state bytes are 92 B/point per launch (12.3 GB at 2^27); "
+                                   "the rest is the per-point pulse tables in local memory "
+                                   "(640 B/thread) moving through L2 (DESIGN.md §5.1)",
                    "executed": {k: K2_PROFILE[k] for k in ("fp64_pipe_active", "issue_active")},
                    "note": "achieved = the reference's flop model (SURVEY 8d F, from the "
                            "kernel's own branch counters over the timed windows) / mean "
@@ -912,6 +1014,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ref-check", action="store_true")
+    ap.add_argument("--no-config3", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--quick", action="store_true", help="skip the secondary measurements")
     ap.add_argument("--plumbing-test", action="store_true", help=argparse.SUPPRESS)
     argv = sys.argv[1:]

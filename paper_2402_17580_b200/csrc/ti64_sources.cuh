@@ -14,6 +14,9 @@
 #include "ti64_fastmath.cuh"
 #include "../../include/ti64_b200.h"
 
+#ifndef PULSE_CACHE
+#define PULSE_CACHE 1
+#endif
 
 namespace ti64 {
 
@@ -61,97 +64,38 @@ __device__ __forceinline__ double add_pulse(double s, double a, double tc, doubl
   return __dadd_rn(s, __dmul_rn(a, exp_core(-uu)));
 }
 
-// live-window half-width of the pulse kinds (g.pf[7], set by the library's
-// entry points from pulse_window_k); 26.7 (u^2 > 708: fast_exp is exactly 0)
-// is exact for any base and amplitude
-__device__ __forceinline__ double window_k(const ti64_tempgen& g) {
-  const double k = (double)g.pf[7];
-  return k > 0.0 ? k : 26.7;
-}
-
-// One point's seeded pulse parameters, regenerated from the
-// counter RNG on demand (bit-identical every time):
-//   config 0 (TI64_SRC_PULSE): p = {A_lo, A_hi, tc_lo, tc_hi, w_lo, w_hi}
-//   config 2 (TI64_SRC_PULSE_TRAIN): p = {A1_lo, A1_hi, j_lo, j_hi, t0, spacing,
-//     tj_lo, tj_hi, w_lo, w_hi, decay, xs_lo, xs_hi}; A_k = (A1 decay^k) U
-//   config 4 (TI64_SRC_PULSE_SWEEP): p = {A_lo, A_hi, c_lo, c_hi, lnw_lo, lnw_hi}
-template <int KIND>
-__device__ __forceinline__ void pulse_params(const ti64_tempgen& g, uint64_t pt, int k,
-                                             double a1, double& a, double& tc, double& w) {
-  if constexpr (KIND == TI64_SRC_PULSE) {
-    a = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
-    tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 1));
-    w = unif(g.p[4], g.p[5], u01(g.seed, pt, 2));
-  } else if constexpr (KIND == TI64_SRC_PULSE_TRAIN) {
-    double scale = 1.0;  // decay^k by repeated multiplication
-    for (int j = 0; j < k; ++j) scale = __dmul_rn(scale, g.p[10]);
-    a = __dmul_rn(__dmul_rn(a1, scale), unif(g.p[2], g.p[3], u01(g.seed, pt, 1 + 3 * k)));
-    tc = __dadd_rn(__dadd_rn(g.p[4], __dmul_rn(g.p[5], (double)k)),
-                   unif(g.p[6], g.p[7], u01(g.seed, pt, 2 + 3 * k)));
-    w = unif(g.p[8], g.p[9], u01(g.seed, pt, 3 + 3 * k));
-  } else {
-    a = unif(g.p[0], g.p[1], u01(g.seed, pt, 1 + 3 * k));
-    tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 2 + 3 * k));
-    w = fast_exp(unif(g.p[4], g.p[5], u01(g.seed, pt, 3 + 3 * k)));
-  }
-}
-
 // Up to MAXP Gaussian pulses per point (configs 0, 2, 4).  Pulse k is only
-// evaluated on steps [lo_k, hi_k] (exact no-op outside, see above); a live
-// mask plus the next step at which it changes keep the per-step cost at the
-// live pulses.  The windows live in (local) memory; the parameters of the
-// lowest live pulse are held in registers and those of up to three more
-// simultaneously live pulses in a small local cache, refilled from the RNG
-// when the live set changes (a fifth live pulse is regenerated per step).
-// Round 1 kept all parameters in local memory: 640 B per thread and ~10x the
-// state bytes of DRAM traffic per launch.
-template <int MAXP, int KIND>
+// evaluated on steps [lo_k, hi_k]; a live mask plus the next step at which
+// it changes keep the per-step cost at the live pulses.
+template <int MAXP>
 struct PulseSet {
-#ifndef PULSE_NC
-#define PULSE_NC 4
-#endif
-  static constexpr int NC = MAXP < PULSE_NC ? MAXP : PULSE_NC;  // live pulses with cached parameters
   double base;
-  double a1;  // config 2: the first pulse's amplitude draw
-  uint64_t pt;
+  double a[MAXP], tc[MAXP], inv_w[MAXP];
   int lo[MAXP], hi[MAXP];
   int np;
   unsigned live;
   int64_t next_event;
-  int ck[NC];            // pulse index of each cache slot (-1: none)
-  double ca0, ctc0, ciw0;  // slot 0 (the lowest live pulse) in registers
-  double cx[NC > 1 ? NC - 1 : 1][3];  // slots 1.. (further live pulses), local
+#if PULSE_CACHE
+  // the lowest live pulse (the first term of the sum) in registers: usually
+  // the only live one, so the per-step sum needs no local-memory loads
+  double ca, ctc, ciw;
+#endif
 
-  // out of line: only rescans (live-set changes) and a fifth live pulse use it
-  __device__ __noinline__ void params(const ti64_tempgen& g, int k, double& a, double& tc,
-                                      double& inv_w) const {
-    double w;
-    pulse_params<KIND>(g, pt, k, a1, a, tc, w);
-    inv_w = div_rn(1.0, w);
+  // wk (> 0): half-width of the live window in widths, from the host
+  // (pulse_window_k): outside it a*fast_exp(-u^2) < ulp(base)/2, an exact no-op
+  __device__ __forceinline__ void add(int k, double ak, double tck, double w, double dt,
+                                      double wk) {
+    a[k] = ak;
+    tc[k] = tck;
+    inv_w[k] = div_rn(1.0, w);
+    // conservative window: outside it |t - tc| >= wk w - O(ulp) (2-step margin)
+    const double l = floor((tck - wk * w) / dt) - 2.0;
+    const double h = ceil((tck + wk * w) / dt) + 2.0;
+    lo[k] = l < -1.0e9 ? -1000000000 : (l > 1.0e9 ? 1000000000 : (int)l);
+    hi[k] = h < -1.0e9 ? -1000000000 : (h > 1.0e9 ? 1000000000 : (int)h);
   }
 
-  __device__ __forceinline__ void init(const ti64_tempgen& g, uint64_t p_, int np_) {
-    base = g.base;
-    pt = p_;
-    np = np_;
-    a1 = KIND == TI64_SRC_PULSE_TRAIN ? unif(g.p[0], g.p[1], u01(g.seed, pt, 0)) : 0.0;
-    const double wk = window_k(g);
-    for (int k = 0; k < np; ++k) {
-      double a, tc, w;
-      pulse_params<KIND>(g, pt, k, a1, a, tc, w);
-      // conservative window: outside it |t - tc| >= wk w - O(ulp) (2-step margin)
-      const double l = floor((tc - wk * w) / g.dt) - 2.0;
-      const double h = ceil((tc + wk * w) / g.dt) + 2.0;
-      lo[k] = l < -1.0e9 ? -1000000000 : (l > 1.0e9 ? 1000000000 : (int)l);
-      hi[k] = h < -1.0e9 ? -1000000000 : (h > 1.0e9 ? 1000000000 : (int)h);
-    }
-    live = 0u;
-    next_event = -1;
-#pragma unroll
-    for (int j = 0; j < NC; ++j) ck[j] = -1;
-  }
-
-  __device__ __forceinline__ void rescan(int64_t n, const ti64_tempgen& g) {
+  __device__ __forceinline__ void rescan(int64_t n) {
     live = 0u;
     int64_t nxt = INT64_MAX;
     for (int k = 0; k < np; ++k) {
@@ -163,88 +107,117 @@ struct PulseSet {
       }
     }
     next_event = nxt;
-    // cache the parameters of the lowest NC live pulses (slot j = j-th live)
-    unsigned m = live;
-    for (int j = 0; j < NC && m; ++j) {
-      const int k = __ffs(m) - 1;
-      m &= m - 1;
-      if (ck[j] == k) continue;
-      if (j == 0 && NC > 1 && ck[1] == k) {  // the lowest live pulse left: shift down
-        ca0 = cx[0][0], ctc0 = cx[0][1], ciw0 = cx[0][2];
-      } else if (j == 0) {
-        params(g, k, ca0, ctc0, ciw0);
-      } else {
-        params(g, k, cx[j - 1][0], cx[j - 1][1], cx[j - 1][2]);
-      }
-      ck[j] = k;
+#if PULSE_CACHE
+    if (live) {
+      const int k = __ffs(live) - 1;
+      ca = a[k];
+      ctc = tc[k];
+      ciw = inv_w[k];
     }
+#endif
   }
 
   // FP32 estimate of T - base (relative error < 1e-5; u is formed in FP64
   // so the only FP32 error is in the exponential and the product).
-  __device__ __forceinline__ float excess_estimate(int64_t n, const ti64_tempgen& g) {
-    if (n >= next_event || n < 0) rescan(n, g);
+  __device__ __forceinline__ float excess_estimate(int64_t n, double dt) {
+    if (n >= next_event || n < 0) rescan(n);
     unsigned m = live;
     if (m == 0u) return 0.0f;
-    const double t = __dmul_rn(step_to_double(n), g.dt);
-    float u = (float)__dmul_rn(__dsub_rn(t, ctc0), ciw0);
-    float e = (float)ca0 * exp2f_approx(-u * u * 1.44269504f);
-    m &= m - 1;
-    for (int j = 1; m; ++j) {
+    const double t = __dmul_rn(step_to_double(n), dt);
+    float e = 0.0f;
+#if PULSE_CACHE
+    {
+      const float u = (float)__dmul_rn(__dsub_rn(t, ctc), ciw);
+      e += (float)ca * exp2f_approx(-u * u * 1.44269504f);
+      m &= m - 1;
+    }
+#endif
+    while (m) {
       const int k = __ffs(m) - 1;
       m &= m - 1;
-      double a, tc, iw;
-      if (j < NC) {
-        a = cx[j - 1][0], tc = cx[j - 1][1], iw = cx[j - 1][2];
-      } else {
-        params(g, k, a, tc, iw);
-      }
-      u = (float)__dmul_rn(__dsub_rn(t, tc), iw);
-      e += (float)a * exp2f_approx(-u * u * 1.44269504f);
+      const float u = (float)__dmul_rn(__dsub_rn(t, tc[k]), inv_w[k]);
+      e += (float)a[k] * exp2f_approx(-u * u * 1.44269504f);
     }
     return e;
   }
 
-  __device__ __forceinline__ double temp(int64_t n, const ti64_tempgen& g) {
-    if (n >= next_event || n < 0) rescan(n, g);
+  __device__ __forceinline__ double temp(int64_t n, double dt) {
+    if (n >= next_event || n < 0) rescan(n);
     double s = base;
     unsigned m = live;
     if (m == 0u) return s;  // every pulse is an exact no-op: T == base
-    const double t = __dmul_rn(step_to_double(n), g.dt);
-    s = add_pulse(s, ca0, ctc0, ciw0, t);  // pulses in increasing k, as the sum is defined
+    const double t = __dmul_rn(step_to_double(n), dt);
+#if PULSE_CACHE
+    s = add_pulse(s, ca, ctc, ciw, t);
     m &= m - 1;
-    for (int j = 1; m; ++j) {
+#endif
+    while (m) {
       const int k = __ffs(m) - 1;
       m &= m - 1;
-      double a, tc, iw;
-      if (j < NC) {
-        a = cx[j - 1][0], tc = cx[j - 1][1], iw = cx[j - 1][2];
-      } else {
-        params(g, k, a, tc, iw);
-      }
-      s = add_pulse(s, a, tc, iw, t);
+      s = add_pulse(s, a[k], tc[k], inv_w[k], t);
     }
     return s;
   }
 };
 
-template <int MAXP, int KIND>
-__device__ __forceinline__ void init_pulse1(PulseSet<MAXP, KIND>& ps, const ti64_tempgen& g,
+// live-window half-width of the pulse kinds (g.pf[7], set by the library's
+// entry points from pulse_window_k); 26.7 (u^2 > 708: fast_exp is exactly 0)
+// is exact for any base and amplitude
+__device__ __forceinline__ double window_k(const ti64_tempgen& g) {
+  const double k = (double)g.pf[7];
+  return k > 0.0 ? k : 26.7;
+}
+
+// config 0 (TI64_SRC_PULSE): p = {A_lo, A_hi, tc_lo, tc_hi, w_lo, w_hi}
+template <int MAXP>
+__device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempgen& g,
                                             uint64_t pt) {
-  ps.init(g, pt, 1);
+  ps.base = g.base;
+  ps.np = 1;
+  const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
+  const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 1));
+  const double w = unif(g.p[4], g.p[5], u01(g.seed, pt, 2));
+  ps.add(0, a, tc, w, g.dt, window_k(g));
+  ps.next_event = -1;
+  ps.live = 0u;
 }
 
-template <int MAXP, int KIND>
-__device__ __forceinline__ void init_train(PulseSet<MAXP, KIND>& ps, const ti64_tempgen& g,
+// config 2 (TI64_SRC_PULSE_TRAIN): p = {A1_lo, A1_hi, j_lo, j_hi, t0, spacing,
+// tj_lo, tj_hi, w_lo, w_hi, decay, xs_lo, xs_hi}
+template <int MAXP>
+__device__ __forceinline__ void init_train(PulseSet<MAXP>& ps, const ti64_tempgen& g,
                                            uint64_t pt) {
-  ps.init(g, pt, g.max_pulses < MAXP ? g.max_pulses : MAXP);
+  ps.base = g.base;
+  ps.np = g.max_pulses < MAXP ? g.max_pulses : MAXP;
+  const double a1 = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
+  double scale = 1.0;
+  for (int k = 0; k < ps.np; ++k) {
+    const double a = __dmul_rn(__dmul_rn(a1, scale), unif(g.p[2], g.p[3], u01(g.seed, pt, 1 + 3 * k)));
+    const double tc = __dadd_rn(__dadd_rn(g.p[4], __dmul_rn(g.p[5], (double)k)),
+                                unif(g.p[6], g.p[7], u01(g.seed, pt, 2 + 3 * k)));
+    const double w = unif(g.p[8], g.p[9], u01(g.seed, pt, 3 + 3 * k));
+    ps.add(k, a, tc, w, g.dt, window_k(g));
+    scale = __dmul_rn(scale, g.p[10]);
+  }
+  ps.next_event = -1;
+  ps.live = 0u;
 }
 
-template <int MAXP, int KIND>
-__device__ __forceinline__ void init_sweep(PulseSet<MAXP, KIND>& ps, const ti64_tempgen& g,
+// config 4 (TI64_SRC_PULSE_SWEEP): p = {A_lo, A_hi, c_lo, c_hi, lnw_lo, lnw_hi}
+template <int MAXP>
+__device__ __forceinline__ void init_sweep(PulseSet<MAXP>& ps, const ti64_tempgen& g,
                                            uint64_t pt) {
-  const int np_ = 1 + (int)__dmul_rn(u01(g.seed, pt, 0), (double)g.max_pulses);
-  ps.init(g, pt, np_ < MAXP ? np_ : MAXP);
+  ps.base = g.base;
+  int np_ = 1 + (int)__dmul_rn(u01(g.seed, pt, 0), (double)g.max_pulses);
+  ps.np = np_ < MAXP ? np_ : MAXP;
+  for (int k = 0; k < ps.np; ++k) {
+    const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 1 + 3 * k));
+    const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 2 + 3 * k));
+    const double w = fast_exp(unif(g.p[4], g.p[5], u01(g.seed, pt, 3 + 3 * k)));
+    ps.add(k, a, tc, w, g.dt, window_k(g));
+  }
+  ps.next_event = -1;
+  ps.live = 0u;
 }
 
 // config 1 (TI64_SRC_ROSENTHAL): p = {coef, v/(2 alpha), cap, arg_noop_f32,
