@@ -82,17 +82,26 @@ struct PulseSet {
 #endif
 
   // wk (> 0): half-width of the live window in widths, from the host
-  // (pulse_window_k): outside it a*fast_exp(-u^2) < ulp(base)/2, an exact no-op
-  __device__ __forceinline__ void add(int k, double ak, double tck, double w, double dt,
-                                      double wk) {
-    a[k] = ak;
-    tc[k] = tck;
-    inv_w[k] = div_rn(1.0, w);
+  // (pulse_window_k): outside it a*fast_exp(-u^2) < ulp(base)/2, an exact no-op.
+  // Only pulses whose live window meets the caller's step range [n_lo, n_hi]
+  // are kept (appended in pulse order, so the sum keeps its association): a
+  // pulse that is never live in the range is never added to the sum, and the
+  // per-thread table (local memory) holds the few pulses of a launch window
+  // instead of every pulse of the point.
+  __device__ __forceinline__ void add(double ak, double tck, double w, double dt, double wk,
+                                      int64_t n_lo, int64_t n_hi) {
     // conservative window: outside it |t - tc| >= wk w - O(ulp) (2-step margin)
     const double l = floor((tck - wk * w) / dt) - 2.0;
     const double h = ceil((tck + wk * w) / dt) + 2.0;
-    lo[k] = l < -1.0e9 ? -1000000000 : (l > 1.0e9 ? 1000000000 : (int)l);
-    hi[k] = h < -1.0e9 ? -1000000000 : (h > 1.0e9 ? 1000000000 : (int)h);
+    const int li = l < -1.0e9 ? -1000000000 : (l > 1.0e9 ? 1000000000 : (int)l);
+    const int hi_ = h < -1.0e9 ? -1000000000 : (h > 1.0e9 ? 1000000000 : (int)h);
+    if ((int64_t)hi_ < n_lo || (int64_t)li > n_hi) return;
+    const int k = np++;
+    a[k] = ak;
+    tc[k] = tck;
+    inv_w[k] = div_rn(1.0, w);
+    lo[k] = li;
+    hi[k] = hi_;
   }
 
   __device__ __forceinline__ void rescan(int64_t n) {
@@ -171,13 +180,13 @@ __device__ __forceinline__ double window_k(const ti64_tempgen& g) {
 // config 0 (TI64_SRC_PULSE): p = {A_lo, A_hi, tc_lo, tc_hi, w_lo, w_hi}
 template <int MAXP>
 __device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempgen& g,
-                                            uint64_t pt) {
+                                            uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
-  ps.np = 1;
+  ps.np = 0;
   const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
   const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 1));
   const double w = unif(g.p[4], g.p[5], u01(g.seed, pt, 2));
-  ps.add(0, a, tc, w, g.dt, window_k(g));
+  ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
   ps.next_event = -1;
   ps.live = 0u;
 }
@@ -186,17 +195,18 @@ __device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempg
 // tj_lo, tj_hi, w_lo, w_hi, decay, xs_lo, xs_hi}
 template <int MAXP>
 __device__ __forceinline__ void init_train(PulseSet<MAXP>& ps, const ti64_tempgen& g,
-                                           uint64_t pt) {
+                                           uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
-  ps.np = g.max_pulses < MAXP ? g.max_pulses : MAXP;
+  const int npt = g.max_pulses < MAXP ? g.max_pulses : MAXP;
+  ps.np = 0;
   const double a1 = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
   double scale = 1.0;
-  for (int k = 0; k < ps.np; ++k) {
+  for (int k = 0; k < npt; ++k) {
     const double a = __dmul_rn(__dmul_rn(a1, scale), unif(g.p[2], g.p[3], u01(g.seed, pt, 1 + 3 * k)));
     const double tc = __dadd_rn(__dadd_rn(g.p[4], __dmul_rn(g.p[5], (double)k)),
                                 unif(g.p[6], g.p[7], u01(g.seed, pt, 2 + 3 * k)));
     const double w = unif(g.p[8], g.p[9], u01(g.seed, pt, 3 + 3 * k));
-    ps.add(k, a, tc, w, g.dt, window_k(g));
+    ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
     scale = __dmul_rn(scale, g.p[10]);
   }
   ps.next_event = -1;
@@ -206,15 +216,16 @@ __device__ __forceinline__ void init_train(PulseSet<MAXP>& ps, const ti64_tempge
 // config 4 (TI64_SRC_PULSE_SWEEP): p = {A_lo, A_hi, c_lo, c_hi, lnw_lo, lnw_hi}
 template <int MAXP>
 __device__ __forceinline__ void init_sweep(PulseSet<MAXP>& ps, const ti64_tempgen& g,
-                                           uint64_t pt) {
+                                           uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
   int np_ = 1 + (int)__dmul_rn(u01(g.seed, pt, 0), (double)g.max_pulses);
-  ps.np = np_ < MAXP ? np_ : MAXP;
-  for (int k = 0; k < ps.np; ++k) {
+  np_ = np_ < MAXP ? np_ : MAXP;
+  ps.np = 0;
+  for (int k = 0; k < np_; ++k) {
     const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 1 + 3 * k));
     const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 2 + 3 * k));
     const double w = fast_exp(unif(g.p[4], g.p[5], u01(g.seed, pt, 3 + 3 * k)));
-    ps.add(k, a, tc, w, g.dt, window_k(g));
+    ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
   }
   ps.next_event = -1;
   ps.live = 0u;

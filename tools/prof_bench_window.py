@@ -1,7 +1,7 @@
 """Profiling driver for the bench headline: config 4 at N points (default
 2^27) prepared to step 20 000 in 5000-step launches (4 advance launches),
-one warm-up window (launch 5), then `--windows` timed 200-step windows (the
-bench's K2 launches).  For ncu: -k regex:advance_kernel --launch-skip 5 -c 1
+one warm-up window (advance launch 101: launches cover at most 200 steps), then `--windows` timed 200-step windows (the
+bench's K2 launches).  For ncu: -k regex:advance_kernel --launch-skip 101 -c 1
 captures the first bench window launch."""
 import argparse
 import sys
