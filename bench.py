@@ -692,10 +692,13 @@ def measure_ode(torch, pkg, cfg_id, K, W, rank, world, dev, dd, *, counted=True,
         d2h = n * (6 * 8 + 2) + sums_h.numel() * 8
         out["e2e"] = {"value": c["n"] * win / t_e2e, "unit": UNIT,
                       "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-                      "path": "GlobalFields(device='host') + advance(): the fused kernel reads "
-                              "each point's inputs from pinned host memory and writes its "
-                              "results back there (zero-copy), timed to the phase sums on the "
-                              "host", "bitwise_equal_to_device_run": bool(same),
+                      "path": "GlobalFields(device='host') + advance() -> ti64_advance_host: "
+                              "the state lives in pinned host memory; chunks of 2^22 points are "
+                              "staged through three device buffers, the host->device copy of "
+                              "the next chunk and the device->host copy of the previous one "
+                              "overlapping each chunk's update; timed from the host arrays to "
+                              "the phase sums and the updated host arrays",
+                      "bitwise_equal_to_device_run": bool(same),
                       "seconds_per_step": t_e2e}
         del host, ref
     # CPU leg: the oracle port on every stride-th point of this shard from the

@@ -36,6 +36,9 @@ _SIGS = {
     "ti64_advance": (_I64, [_P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                             _P, _P]),
     "ti64_advance_scratch_bytes": (_I64, [_I64]),
+    "ti64_advance_host": (_I64, [_P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
+                                 _P, _I64, _I64, _P]),
+    "ti64_advance_host_scratch_bytes": (_I64, [_I64, _I64, _I64, _I64]),
     "ti64_run_history": (_I64, [_P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
     "ti64_fast_exp": (_I64, [_P, _P, _I64, _P]),
     "ti64_fast_ln": (_I64, [_P, _P, _I64, _P]),

@@ -79,11 +79,11 @@ class GlobalFields:
     resident on the GPU (batch.py:99-146).
 
     device="host" keeps them in pinned host memory instead, mapped into the
-    GPU's address space: the kernels then read their inputs from and write
-    their results to host memory themselves (zero-copy).  For the fused
-    advance, which touches each point's state once at the start and once at
-    the end of the launch, the host-link transfer overlaps the computation
-    of other points — the end-to-end path for data that lives on the host.
+    GPU's address space.  step_all then reads its inputs from and writes its
+    results to host memory itself (zero-copy, coalesced); the fused advance
+    stages chunks of points through device buffers with the copies of the
+    neighbouring chunks overlapping each chunk's update (ti64_advance_host) —
+    the end-to-end path for data that lives on the host.
     Host reads (states/host/to_host) synchronise the device first."""
 
     x_alpha_s: object
@@ -340,7 +340,7 @@ def _scratch(n, device):
 
 def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
             config=IntegratorConfig(), n_lanes=8, snapshot_every=0, counters=None,
-            point_offset=0, stream=None, scratch=None):
+            point_offset=0, stream=None, scratch=None, host_chunk_points=0):
     """Fused advance (K2): equivalent, bit for bit, to
 
         for s in range(step0, step0 + n_steps):
@@ -350,6 +350,13 @@ def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
     with per-point state held in registers across steps.  Returns an
     AdvanceResult whose ``sums`` are the phase-fraction sums after every
     `snapshot_every` steps (and at the end).
+
+    Host-resident fields (``GlobalFields(..., device="host")``) go through
+    ti64_advance_host: chunks of `host_chunk_points` points (0: the library's
+    default) are staged through device buffers with the host<->device copies
+    overlapping the update; ``host_chunk_points=-1`` keeps the zero-copy
+    access of the mapped host arrays instead (the scratch argument only
+    applies there and to device-resident fields).
     """
     if n_lanes not in SUPPORTED_LANES:
         raise ValueError(f"n_lanes must be one of {SUPPORTED_LANES}")
@@ -367,15 +374,29 @@ def advance(fields, n_steps, source, step0=0, params=DEFAULT_PARAMS,
     chunk = snapshot_every if snapshot_every > 0 else max(n_steps, 1)
     n_snap = (n_steps + chunk - 1) // chunk if n_steps > 0 else 0
     sums = torch.zeros((max(n_snap, 1), 3), dtype=torch.float64, device=dev)
-    scratch = _scratch(n, dev) if scratch is None else scratch
     cs = counters.cstruct() if counters is not None else None
     fs = fields.cstruct()
     kp, cfg = _kp(params), _cfg(config)
-    rc = lib.ti64_advance(C.byref(fs), n, C.byref(g), int(step0), int(n_steps), int(nsub),
-                          int(n_lanes), int(snapshot_every), C.byref(kp), C.byref(cfg),
-                          None if cs is None else C.byref(cs), _lib.ptr(sums),
-                          _lib.ptr(scratch), _lib.stream_handle(stream))
-    launches = _lib.check(rc, "ti64_advance")  # >= 0: kernels launched
+    if fields.host_resident and host_chunk_points >= 0:
+        # host arrays: chunks staged through device buffers, the copies of the
+        # neighbouring chunks overlapping each chunk's update (ti64_advance_host)
+        nbytes = int(_lib.check(lib.ti64_advance_host_scratch_bytes(
+            n, int(host_chunk_points), int(n_steps), int(snapshot_every)),
+            "ti64_advance_host_scratch_bytes"))
+        scratch = torch.empty((nbytes + 7) // 8, dtype=torch.float64, device=dev)
+        rc = lib.ti64_advance_host(C.byref(fs), n, C.byref(g), int(step0), int(n_steps),
+                                   int(nsub), int(n_lanes), int(snapshot_every), C.byref(kp),
+                                   C.byref(cfg), None if cs is None else C.byref(cs),
+                                   _lib.ptr(sums), _lib.ptr(scratch), nbytes,
+                                   int(host_chunk_points), _lib.stream_handle(stream))
+        launches = _lib.check(rc, "ti64_advance_host")
+    else:
+        scratch = _scratch(n, dev) if scratch is None else scratch
+        rc = lib.ti64_advance(C.byref(fs), n, C.byref(g), int(step0), int(n_steps), int(nsub),
+                              int(n_lanes), int(snapshot_every), C.byref(kp), C.byref(cfg),
+                              None if cs is None else C.byref(cs), _lib.ptr(sums),
+                              _lib.ptr(scratch), _lib.stream_handle(stream))
+        launches = _lib.check(rc, "ti64_advance")  # >= 0: kernels launched
     _keep_for_stream(stream, beam, sums, scratch)
     del beam
     fields.traffic_bytes += BYTES_PER_POINT * n * n_steps

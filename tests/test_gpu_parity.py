@@ -412,6 +412,35 @@ def test_phase_sums_and_histogram(pkg):
         assert np.array_equal(hist[c], ref)
 
 
+@pytest.mark.parametrize("cfg_id,n,steps,chunk", [(4, 150_013, 450, 4096), (4, 70_000, 300, 65536),
+                                                   (2, 90_001, 400, 8192), (0, 5000, 600, 1024),
+                                                   (1, 32768, 300, 5000)])
+@pytest.mark.parametrize("lanes", [8, 1])
+def test_host_fields_staged_chunks(pkg, cfg_id, n, steps, chunk, lanes):
+    """ti64_advance_host: host arrays staged through the device in chunks
+    (ragged last chunk, chunk sizes rounded to 1024, a window starting
+    mid-job) give the bits of one device-resident advance over all points,
+    event counters included; the zero-copy form of the same call agrees too."""
+    src = pkg.source_for_config(cfg_id) if cfg_id != 1 else pkg.RosenthalRaster(nx=64, ny=64, nz=8)
+    a = pkg.init_from_source(src, n, point_offset=37 * 32)
+    pkg.advance(a, 250, src, point_offset=37 * 32, n_lanes=lanes)  # off the initial state
+    start = a.to_host()
+    ca = pkg.EventCounters(n, a.device)
+    ra = pkg.advance(a, steps, src, step0=250, point_offset=37 * 32, n_lanes=lanes,
+                     snapshot_every=170, counters=ca)
+    want = a.to_host()
+    for hc in (chunk, -1):
+        h = pkg.GlobalFields(*[start[k] for k in FIELD_NAMES], device="host")
+        ch = pkg.EventCounters(n, a.device)
+        rh = pkg.advance(h, steps, src, step0=250, point_offset=37 * 32, n_lanes=lanes,
+                         snapshot_every=170, counters=ch, host_chunk_points=hc)
+        assert_fields(h, want, f"host chunks {hc}")
+        np.testing.assert_allclose(rh.sums.cpu().numpy(), ra.sums.cpu().numpy(), rtol=1e-12)
+        assert ch.totals_dict() == ca.totals_dict()
+        assert np.array_equal(ch.martensite.cpu().numpy(), ca.martensite.cpu().numpy())
+        assert np.array_equal(ch.switches.cpu().numpy(), ca.switches.cpu().numpy())
+
+
 def test_host_resident_fields_zero_copy(pkg):
     """GlobalFields(device='host'): pinned host state read and written by the
     kernels themselves gives the same bits as device-resident state."""
