@@ -56,12 +56,13 @@ __device__ __forceinline__ double step_to_double(int64_t n) {
 
 // Gaussian pulse contribution a*fast_exp(-u^2), u = (t - tc)*inv_w.
 // -u*u is never NaN and <= 0; below -708 fast_exp is exactly 0.
+template <class C = CoefBank>
 __device__ __forceinline__ double add_pulse(double s, double a, double tc, double inv_w,
-                                            double t) {
+                                            double t, const C& c = C()) {
   const double u = __dmul_rn(__dsub_rn(t, tc), inv_w);
   const double uu = __dmul_rn(u, u);
   if (uu > 708.0) return __dadd_rn(s, 0.0);  // a * 0.0 == +0.0
-  return __dadd_rn(s, __dmul_rn(a, exp_core(-uu)));
+  return __dadd_rn(s, __dmul_rn(a, exp_core(-uu, c)));
 }
 
 // Up to MAXP Gaussian pulses per point (configs 0, 2, 4).  Pulse k is only
@@ -150,20 +151,21 @@ struct PulseSet {
     return e;
   }
 
-  __device__ __forceinline__ double temp(int64_t n, double dt) {
+  template <class C = CoefBank>
+  __device__ __forceinline__ double temp(int64_t n, double dt, const C& c = C()) {
     if (n >= next_event || n < 0) rescan(n);
     double s = base;
     unsigned m = live;
     if (m == 0u) return s;  // every pulse is an exact no-op: T == base
     const double t = __dmul_rn(step_to_double(n), dt);
 #if PULSE_CACHE
-    s = add_pulse(s, ca, ctc, ciw, t);
+    s = add_pulse(s, ca, ctc, ciw, t, c);
     m &= m - 1;
 #endif
     while (m) {
       const int k = __ffs(m) - 1;
       m &= m - 1;
-      s = add_pulse(s, a[k], tc[k], inv_w[k], t);
+      s = add_pulse(s, a[k], tc[k], inv_w[k], t, c);
     }
     return s;
   }
