@@ -73,10 +73,10 @@ F_BASE, F_FORM, F_GA, F_GROW, F_AM, F_DIS, F_TAIL = 48, 22, 46, 49, 49, 98, 18
 # executed view and DRAM traffic of the headline launch, from the committed
 # ncu capture of the bench workload (profiles/README.md, round 2)
 K2_PROFILE = {
-    "file": "profiles/r02a_advance_cfg4_window.txt (ncu --set full of the first timed window "
-            "launch, 2^27 points, steps 20200-20400)",
-    "dram_bytes_per_launch": 38_838_518_000 + 79_459_955_000,  # read + write
-    "fp64_pipe_active": 0.5255, "issue_active": 0.8029,
+    "file": "profiles/r02e_advance_cfg4_window.txt (ncu --set full of the first timed window "
+            "launch at HEAD, 2^27 points, steps 20200-20400)",
+    "dram_bytes_per_launch": 32_226_234_000 + 23_052_263_000,  # read + write
+    "fp64_pipe_active": 0.5195, "issue_active": 0.7253,
 }
 
 
@@ -941,8 +941,11 @@ def run_b200(args):
                    "traffic": K2_PROFILE["dram_bytes_per_launch"],
                    "traffic_source": K2_PROFILE["file"],
                    "traffic_note": "state bytes are 92 B/point per launch (12.3 GB at 2^27); "
-                                   "the rest is the per-point pulse tables in local memory "
-                                   "(640 B/thread) moving through L2 (DESIGN.md §5.1)",
+                                   "the rest is sector amplification of the 8-byte gathers / "
+                                   "scatters in work-class order (each 32-byte sector is "
+                                   "touched once per class present in it) and the per-thread "
+                                   "pulse tables in local memory; 0.13 TB/s in total, far from "
+                                   "the HBM bound (DESIGN.md §5.2)",
                    "executed": {k: K2_PROFILE[k] for k in ("fp64_pipe_active", "issue_active")},
                    "note": "achieved = the reference's flop model (SURVEY 8d F, from the "
                            "kernel's own branch counters over the timed windows) / mean "
