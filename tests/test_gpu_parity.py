@@ -374,6 +374,38 @@ def test_advance_pulse_throughput_instance_vs_oracle(pkg, orc, cfg_id, step0, ns
         assert_bitwise(h[k][8192:8192 + 4096], hs[k], f"cfg{cfg_id} lat-vs-throughput:{k}")
 
 
+@pytest.mark.parametrize("over", [dict(k3=0.2), dict(k1=0.5, k2=700.0, k_alpha_m_eq=0.01),
+                                  dict(t_alpha_s_end=1300.0)])
+@pytest.mark.parametrize("cfg_id,step0", [(4, 20000), (2, 10000)])
+def test_advance_cold_loop_other_parameters_vs_oracle(pkg, orc, cfg_id, step0, over):
+    """The cold loop of K2 with kinetics parameters other than the defaults:
+    k3 = 0.2 puts k_alpha_s's exponential argument outside the host-verified
+    range (the loop then keeps fast_exp's and the division's range branches),
+    the second set stays inside it with other values, the third has
+    T_alpha_s,end above T_alpha_s,start (no range rest, no cold loop).
+    Throughput-instance launch, mid-job states; two blocks against the oracle."""
+    from paper_2402_17580_b200.batch import gen_temperature
+    params = pkg.DEFAULT_PARAMS.with_overrides(**over)
+    src = pkg.source_for_config(cfg_id)
+    n, pre, nsteps = 1 << 16, 1500, 700
+    f = pkg.init_from_source(src, n)
+    f.temperature_old.copy_(gen_temperature(src, n, step0))
+    pkg.advance(f, pre, src, step0=step0, params=params)
+    pkg.advance(f, nsteps, src, step0=step0 + pre, params=params, snapshot_every=300)
+    h = f.to_host()
+    kp = params.kernel_tuple()
+    cfg = pkg.IntegratorConfig().kernel_tuple()
+    for off in (4096, n - 2048):
+        g = src.tempgen(point_offset=off)
+        ho = orc.gen_initial_state(g, 2048)
+        t0 = orc.gen_temperature(g, 2048, step0)
+        ho.temperature_old[:] = t0
+        ho.temperature_new[:] = t0
+        orc.advance(ho, g, step0, pre + nsteps, kp, cfg, lanes=8, threads=8)
+        for k in FIELD_NAMES:
+            assert_bitwise(h[k][off:off + 2048], getattr(ho, k), f"cfg{cfg_id} {over} {off}:{k}")
+
+
 def test_full_config1_invariants(pkg):
     """Size-independent properties at BASELINE config 1's full size and
     length: continuity sum == 1 - g(T) (acceptance criterion 3, <= 1e-12),
