@@ -70,6 +70,7 @@ __device__ __forceinline__ double add_pulse(double s, double a, double tc, doubl
 // it changes keep the per-step cost at the live pulses.
 template <int MAXP>
 struct PulseSet {
+  static constexpr int MAX_PULSES = MAXP;
   double base;
   double a[MAXP], tc[MAXP], inv_w[MAXP];
   int lo[MAXP], hi[MAXP];
@@ -171,6 +172,33 @@ struct PulseSet {
   }
 };
 
+// A pulse visitor with PulseSet's add() signature for the work-class order of
+// the fused advance: "will this point get hot (T near T_alpha_s,end or above)
+// within the coming launch window?"  A pulse of amplitude above `thr` reaches
+// base + thr inside |t - t_c| <= rw w (rw from the largest amplitude, host
+// side).  Only a scheduling hint: overlapping smaller pulses are ignored and
+// no result depends on it.
+template <int MAXP>
+struct HotProbe {
+  static constexpr int MAX_PULSES = MAXP;
+  double base;
+  int np;
+  unsigned live;
+  int64_t next_event;
+  double thr, rw, t_lo, t_hi;
+  float inv_thr;
+  bool hot;
+  __device__ __forceinline__ void add(double ak, double tck, double w, double, double, int64_t,
+                                      int64_t) {
+    if (ak > thr) {
+      // radius of the pulse's own amplitude (FP32: a hint), capped by rw
+      const float q = sqrtf(__logf((float)ak * inv_thr)) * 1.02f + 0.02f;
+      const double r = (double)fminf(q, (float)rw) * w;
+      hot |= (tck + r >= t_lo) & (tck - r <= t_hi);
+    }
+  }
+};
+
 // live-window half-width of the pulse kinds (g.pf[7], set by the library's
 // entry points from pulse_window_k); 26.7 (u^2 > 708: fast_exp is exactly 0)
 // is exact for any base and amplitude
@@ -180,8 +208,8 @@ __device__ __forceinline__ double window_k(const ti64_tempgen& g) {
 }
 
 // config 0 (TI64_SRC_PULSE): p = {A_lo, A_hi, tc_lo, tc_hi, w_lo, w_hi}
-template <int MAXP>
-__device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempgen& g,
+template <class PS>
+__device__ __forceinline__ void init_pulse1(PS& ps, const ti64_tempgen& g,
                                             uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
   ps.np = 0;
@@ -195,11 +223,11 @@ __device__ __forceinline__ void init_pulse1(PulseSet<MAXP>& ps, const ti64_tempg
 
 // config 2 (TI64_SRC_PULSE_TRAIN): p = {A1_lo, A1_hi, j_lo, j_hi, t0, spacing,
 // tj_lo, tj_hi, w_lo, w_hi, decay, xs_lo, xs_hi}
-template <int MAXP>
-__device__ __forceinline__ void init_train(PulseSet<MAXP>& ps, const ti64_tempgen& g,
+template <class PS>
+__device__ __forceinline__ void init_train(PS& ps, const ti64_tempgen& g,
                                            uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
-  const int npt = g.max_pulses < MAXP ? g.max_pulses : MAXP;
+  const int npt = g.max_pulses < PS::MAX_PULSES ? g.max_pulses : PS::MAX_PULSES;
   ps.np = 0;
   const double a1 = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
   double scale = 1.0;
@@ -216,12 +244,12 @@ __device__ __forceinline__ void init_train(PulseSet<MAXP>& ps, const ti64_tempge
 }
 
 // config 4 (TI64_SRC_PULSE_SWEEP): p = {A_lo, A_hi, c_lo, c_hi, lnw_lo, lnw_hi}
-template <int MAXP>
-__device__ __forceinline__ void init_sweep(PulseSet<MAXP>& ps, const ti64_tempgen& g,
+template <class PS>
+__device__ __forceinline__ void init_sweep(PS& ps, const ti64_tempgen& g,
                                            uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
   int np_ = 1 + (int)__dmul_rn(u01(g.seed, pt, 0), (double)g.max_pulses);
-  np_ = np_ < MAXP ? np_ : MAXP;
+  np_ = np_ < PS::MAX_PULSES ? np_ : PS::MAX_PULSES;
   ps.np = 0;
   for (int k = 0; k < np_; ++k) {
     const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 1 + 3 * k));
