@@ -176,8 +176,9 @@ struct PulseSet {
 // the fused advance: "will this point get hot (T near T_alpha_s,end or above)
 // within the coming launch window?"  A pulse of amplitude above `thr` reaches
 // base + thr inside |t - t_c| <= rw w (rw from the largest amplitude, host
-// side).  Only a scheduling hint: overlapping smaller pulses are ignored and
-// no result depends on it.
+// side); live_soon: some pulse is live (off the base temperature) within the
+// window.  Only scheduling hints: overlapping smaller pulses are ignored and
+// no result depends on them.
 template <int MAXP>
 struct HotProbe {
   static constexpr int MAX_PULSES = MAXP;
@@ -187,9 +188,11 @@ struct HotProbe {
   int64_t next_event;
   double thr, rw, t_lo, t_hi;
   float inv_thr;
-  bool hot;
-  __device__ __forceinline__ void add(double ak, double tck, double w, double, double, int64_t,
-                                      int64_t) {
+  bool hot, live_soon;
+  __device__ __forceinline__ void add(double ak, double tck, double w, double, double wk,
+                                      int64_t, int64_t) {
+    const double rl = wk * w;  // the live window (PulseSet::add), without its 2-step margin
+    live_soon |= (tck + rl >= t_lo) & (tck - rl <= t_hi);
     if (ak > thr) {
       // radius of the pulse's own amplitude (FP32: a hint), capped by rw
       const float q = sqrtf(__logf((float)ak * inv_thr)) * 1.02f + 0.02f;
