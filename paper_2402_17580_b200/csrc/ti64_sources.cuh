@@ -32,6 +32,15 @@ __device__ __forceinline__ double u01(uint64_t seed, uint64_t point, uint64_t k)
   return __dmul_rn(__ull2double_rn(b >> 11), 0x1.0p-53);
 }
 
+// u01 with the point's key h = splitmix(seed ^ splitmix(point)) formed once
+__device__ __forceinline__ uint64_t point_key(uint64_t seed, uint64_t point) {
+  return splitmix(seed ^ splitmix(point));
+}
+__device__ __forceinline__ double u01_keyed(uint64_t h, uint64_t k) {
+  const uint64_t b = splitmix(h ^ (k * 0xD1B54A32D192ED03ULL));
+  return __dmul_rn(__ull2double_rn(b >> 11), 0x1.0p-53);
+}
+
 __device__ __forceinline__ double unif(double lo, double hi, double u) {
   return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u));
 }
@@ -210,16 +219,29 @@ __device__ __forceinline__ double window_k(const ti64_tempgen& g) {
   return k > 0.0 ? k : 26.7;
 }
 
+// A pulse centred farther than g.pf[6] seconds (the library's bound on the
+// live half-width wk w of any pulse of the generator, + 4 steps; 0: unknown)
+// from the step range [n_lo, n_hi] is not live anywhere in it: add() would
+// drop it, so its amplitude and width need not be drawn at all.
+__device__ __forceinline__ bool pulse_out_of_reach(double tc, const ti64_tempgen& g,
+                                                   int64_t n_lo, int64_t n_hi) {
+  const double reach = (double)g.pf[6];
+  return (reach > 0.0) & ((tc + reach < __dmul_rn((double)n_lo, g.dt)) |
+                          (tc - reach > __dmul_rn((double)n_hi, g.dt)));
+}
+
 // config 0 (TI64_SRC_PULSE): p = {A_lo, A_hi, tc_lo, tc_hi, w_lo, w_hi}
 template <class PS>
 __device__ __forceinline__ void init_pulse1(PS& ps, const ti64_tempgen& g,
                                             uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
   ps.np = 0;
-  const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
   const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 1));
-  const double w = unif(g.p[4], g.p[5], u01(g.seed, pt, 2));
-  ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
+  if (!pulse_out_of_reach(tc, g, n_lo, n_hi)) {
+    const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
+    const double w = unif(g.p[4], g.p[5], u01(g.seed, pt, 2));
+    ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
+  }
   ps.next_event = -1;
   ps.live = 0u;
 }
@@ -235,11 +257,14 @@ __device__ __forceinline__ void init_train(PS& ps, const ti64_tempgen& g,
   const double a1 = unif(g.p[0], g.p[1], u01(g.seed, pt, 0));
   double scale = 1.0;
   for (int k = 0; k < npt; ++k) {
-    const double a = __dmul_rn(__dmul_rn(a1, scale), unif(g.p[2], g.p[3], u01(g.seed, pt, 1 + 3 * k)));
     const double tc = __dadd_rn(__dadd_rn(g.p[4], __dmul_rn(g.p[5], (double)k)),
                                 unif(g.p[6], g.p[7], u01(g.seed, pt, 2 + 3 * k)));
-    const double w = unif(g.p[8], g.p[9], u01(g.seed, pt, 3 + 3 * k));
-    ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
+    if (!pulse_out_of_reach(tc, g, n_lo, n_hi)) {
+      const double a = __dmul_rn(__dmul_rn(a1, scale),
+                                 unif(g.p[2], g.p[3], u01(g.seed, pt, 1 + 3 * k)));
+      const double w = unif(g.p[8], g.p[9], u01(g.seed, pt, 3 + 3 * k));
+      ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
+    }
     scale = __dmul_rn(scale, g.p[10]);
   }
   ps.next_event = -1;
@@ -251,13 +276,25 @@ template <class PS>
 __device__ __forceinline__ void init_sweep(PS& ps, const ti64_tempgen& g,
                                            uint64_t pt, int64_t n_lo, int64_t n_hi) {
   ps.base = g.base;
-  int np_ = 1 + (int)__dmul_rn(u01(g.seed, pt, 0), (double)g.max_pulses);
+  const uint64_t h = point_key(g.seed, pt);
+  int np_ = 1 + (int)__dmul_rn(u01_keyed(h, 0), (double)g.max_pulses);
   np_ = np_ < PS::MAX_PULSES ? np_ : PS::MAX_PULSES;
   ps.np = 0;
+  // pass 1: the centres only (one draw per pulse); pass 2: each lane draws
+  // amplitude and width of ITS pulses within reach, in pulse order -- lanes
+  // work on different pulses at once instead of every lane waiting through
+  // all 20 pulse slots for the few lanes that need one (MAX_PULSES <= 32)
+  unsigned near = 0u;
   for (int k = 0; k < np_; ++k) {
-    const double a = unif(g.p[0], g.p[1], u01(g.seed, pt, 1 + 3 * k));
-    const double tc = unif(g.p[2], g.p[3], u01(g.seed, pt, 2 + 3 * k));
-    const double w = fast_exp(unif(g.p[4], g.p[5], u01(g.seed, pt, 3 + 3 * k)));
+    const double tc = unif(g.p[2], g.p[3], u01_keyed(h, 2 + 3 * k));
+    if (!pulse_out_of_reach(tc, g, n_lo, n_hi)) near |= 1u << k;
+  }
+  while (near) {
+    const int k = __ffs(near) - 1;
+    near &= near - 1u;
+    const double tc = unif(g.p[2], g.p[3], u01_keyed(h, 2 + 3 * k));
+    const double a = unif(g.p[0], g.p[1], u01_keyed(h, 1 + 3 * k));
+    const double w = fast_exp(unif(g.p[4], g.p[5], u01_keyed(h, 3 + 3 * k)));
     ps.add(a, tc, w, g.dt, window_k(g), n_lo, n_hi);
   }
   ps.next_event = -1;
