@@ -73,10 +73,12 @@ F_BASE, F_FORM, F_GA, F_GROW, F_AM, F_DIS, F_TAIL = 48, 22, 46, 49, 49, 98, 18
 # executed view and DRAM traffic of the headline launch, from the committed
 # ncu capture of the bench workload (profiles/README.md, round 2)
 K2_PROFILE = {
-    "file": "profiles/r02e_advance_cfg4_window.txt (ncu --set full of the first timed window "
+    "file": "profiles/r02j_advance_cfg4_window.txt (ncu --set full of the first timed window "
             "launch at HEAD, 2^27 points, steps 20200-20400)",
-    "dram_bytes_per_launch": 32_226_234_000 + 23_052_263_000,  # read + write
-    "fp64_pipe_active": 0.5195, "issue_active": 0.7253,
+    "dram_bytes_per_launch": 32_572_674_000 + 22_809_946_000,  # read + write
+    "fp64_pipe_active": 0.5963, "issue_active": 0.7881,
+    # FP64-pipe warp instructions per 32 point-updates (DFMA+DADD+DMUL+DSETP+FRND) of that launch
+    "fp64_inst_per_update": 134.8,
 }
 
 
@@ -946,7 +948,14 @@ def run_b200(args):
                                    "touched once per class present in it) and the per-thread "
                                    "pulse tables in local memory; 0.13 TB/s in total, far from "
                                    "the HBM bound (DESIGN.md §5.2)",
-                   "executed": {k: K2_PROFILE[k] for k in ("fp64_pipe_active", "issue_active")},
+                   "executed": {k: K2_PROFILE[k] for k in ("fp64_pipe_active", "issue_active",
+                                                            "fp64_inst_per_update")},
+                   "ceiling_at_saturated_fp64_pipe": rl["flops_per_update"] /
+                   (2.0 * K2_PROFILE["fp64_inst_per_update"]),
+                   "ceiling_note": "the bit-exact instruction stream has fp64_inst_per_update "
+                                   "FP64-pipe instructions per update, of which only the DFMAs "
+                                   "carry two flops: frac cannot exceed flops_per_update / (2 x "
+                                   "that) even with the FP64 pipe 100 % busy (DESIGN.md §5.2)",
                    "note": "achieved = the reference's flop model (SURVEY 8d F, from the "
                            "kernel's own branch counters over the timed windows) / mean "
                            "launch time; per GPU"})
