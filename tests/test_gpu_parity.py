@@ -473,6 +473,50 @@ def test_host_fields_staged_chunks(pkg, cfg_id, n, steps, chunk, lanes):
         assert np.array_equal(ch.switches.cpu().numpy(), ca.switches.cpu().numpy())
 
 
+def test_advance_host_c_abi_contract(pkg):
+    """ti64_advance_host through ctypes: scratch-size query, argument errors
+    (negative return + message, host arrays untouched), empty input, and
+    pageable (unpinned) host arrays giving the same bits as pinned ones."""
+    import ctypes as C
+
+    import torch
+    from paper_2402_17580_b200 import _lib
+    from paper_2402_17580_b200.batch import _cfg, _kp
+    lib = _lib.require()
+    src = pkg.source_for_config(4)
+    n = 50_000
+    a = pkg.init_from_source(src, n)
+    pkg.advance(a, 300, src)
+    start = a.to_host()
+    pkg.advance(a, 200, src, step0=300)
+    want = a.to_host()
+    g = src.tempgen(point_offset=0)
+    kp, cfg = _kp(pkg.DEFAULT_PARAMS), _cfg(pkg.IntegratorConfig())
+    need = lib.ti64_advance_host_scratch_bytes(n, 8192, 200, 0)
+    assert need > 3 * 50 * 8192
+    assert lib.ti64_advance_host_scratch_bytes(-1, 0, 1, 0) < 0
+    scratch = torch.empty(need // 8 + 1, dtype=torch.float64, device="cuda")
+    arrs = [np.array(start[k], copy=True) for k in FIELD_NAMES]  # pageable numpy memory
+    f = _lib._abi.Fields(*[x.ctypes.data for x in arrs])
+    st = _lib.stream_handle()
+
+    def call(nn, staging, nbytes, lanes=8):
+        return lib.ti64_advance_host(C.byref(f), nn, C.byref(g), 300, 200, 1, lanes, 0,
+                                     C.byref(kp), C.byref(cfg), None, None, staging, nbytes,
+                                     8192, st)
+    assert call(n, _lib.ptr(scratch), need - 1) == -1      # staging too small
+    assert b"staging" in lib.ti64_last_error()
+    assert call(n, None, need) == -1                        # no staging
+    assert call(n, _lib.ptr(scratch), need, lanes=3) == -1  # bad lane width
+    for x, k in zip(arrs, FIELD_NAMES):
+        assert_bitwise(x, start[k], f"untouched after errors:{k}")
+    assert call(0, _lib.ptr(scratch), need) == 0            # empty input
+    assert call(n, _lib.ptr(scratch), need) > 0
+    torch.cuda.synchronize()
+    for x, k in zip(arrs, FIELD_NAMES):
+        assert_bitwise(x, want[k], f"pageable host arrays:{k}")
+
+
 def test_host_resident_fields_zero_copy(pkg):
     """GlobalFields(device='host'): pinned host state read and written by the
     kernels themselves gives the same bits as device-resident state."""
