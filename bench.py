@@ -73,12 +73,12 @@ F_BASE, F_FORM, F_GA, F_GROW, F_AM, F_DIS, F_TAIL = 48, 22, 46, 49, 49, 98, 18
 # executed view and DRAM traffic of the headline launch, from the committed
 # ncu capture of the bench workload (profiles/README.md, round 2)
 K2_PROFILE = {
-    "file": "profiles/r02j_advance_cfg4_window.txt (ncu --set full of the first timed window "
+    "file": "profiles/r02l_advance_cfg4_window.txt (ncu --set full of the first timed window "
             "launch at HEAD, 2^27 points, steps 20200-20400)",
-    "dram_bytes_per_launch": 32_572_674_000 + 22_809_946_000,  # read + write
-    "fp64_pipe_active": 0.5963, "issue_active": 0.7881,
+    "dram_bytes_per_launch": 33_225_701_000 + 22_913_592_000,  # read + write
+    "fp64_pipe_active": 0.5934, "issue_active": 0.7855,
     # FP64-pipe warp instructions per 32 point-updates (DFMA+DADD+DMUL+DSETP+FRND) of that launch
-    "fp64_inst_per_update": 134.8,
+    "fp64_inst_per_update": 130.9,
 }
 
 
