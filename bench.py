@@ -842,6 +842,24 @@ def measure_extra(torch, pkg, dev, dd, peak_tf, args):
         ts.append((m, a.elapsed_time(b) * 1e-3))
         s3 += m
     tot = sum(x for _, x in ts)
+    # end to end for a job whose fields start and end in host memory: the
+    # state is uploaded once and downloaded once around the 20 000 steps
+    pin = {k: torch.empty(getattr(dom.fields, k).shape, dtype=getattr(dom.fields, k).dtype,
+                          pin_memory=True) for k in pkg.batch.NAMES}
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    for k in pkg.batch.NAMES:
+        pin[k].copy_(getattr(dom.fields, k), non_blocking=True)
+    torch.cuda.synchronize()
+    t_d2h = time.perf_counter() - c0
+    up = {k: torch.empty_like(getattr(dom.fields, k)) for k in pkg.batch.NAMES}
+    c0 = time.perf_counter()
+    for k in pkg.batch.NAMES:
+        up[k].copy_(pin[k], non_blocking=True)
+    torch.cuda.synchronize()
+    t_h2d = time.perf_counter() - c0
+    bytes3 = sum(v.numel() * v.element_size() for v in pin.values())
+    del up, pin
     h3 = dom.fields.to_host()
     cpu3 = None
     if not args.no_cpu_baseline:  # one full-grid step on the host (port)
@@ -873,6 +891,15 @@ def measure_extra(torch, pkg, dev, dd, peak_tf, args):
         "T_max_end": float(h3["temperature_old"].max()),
         "transformed_cells_end": int(np.count_nonzero(h3["x_alpha_s"] != 0.9)),
         "path": "split coupled step: K4 + hot-row bitmap, row scan, kinetics of listed rows",
+        "roofline": {"bound": "hbm", "achieved": 16 * n * (job3 - 1) / tot / 1e9, "peak": hbm,
+                     "unit": "GB/s", "frac": 16 * n * (job3 - 1) / tot / 1e9 / hbm,
+                     "note": "16 B/cell-step (T_n read, T_n+1 written); the kinetics state of "
+                             "idle rows is not touched (1/64 B/cell idle map)"},
+        "e2e": {"value": n * (job3 - 1) / (tot + t_h2d + t_d2h), "unit": "cell-steps/s",
+                "h2d_bytes_per_job": bytes3, "d2h_bytes_per_job": bytes3,
+                "h2d_seconds": t_h2d, "d2h_seconds": t_d2h,
+                "path": "fields uploaded once from pinned host memory, 20 000 coupled steps "
+                        "on the device, fields downloaded once (copies timed on this box)"},
         "cpu_baseline": cpu3}
     del dom, flush, h3
     # K1 (one step_all) at 2^26 cold points: the HBM-bound per-step kernel
