@@ -51,6 +51,8 @@ _SIGS = {
     "ti64_bench_dfma": (_I64, [_P, _I64, _I32, _P]),
     "ti64_bench_daxpy": (_I64, [_P, _P, _D, _I64, _P]),
     "ti64_coupled_step": (_I64, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64, _I32, _P]),
+    "ti64_coupled_step_streams": (_I64, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64, _I32,
+                                         _P, _P]),
     "ti64_coupled_scratch_words": (_I64, [_I64]),
     "ti64_step_counter_add": (_I64, [_P, _I64, _P]),
     "ti64_last_error": (C.c_char_p, []),

@@ -920,12 +920,11 @@ extern "C" int64_t ti64_coupled_scratch_words(int64_t n_cells) {
   return (nrows + 31) / 32 + 4 + nrows;
 }
 
-extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti64_fields* f,
-                                     int64_t state_z0, uint32_t* idle_bits_d,
-                                     uint32_t* scratch_d, const ti64_thermal* tp,
-                                     const ti64_stencil_args* a, const ti64_kparams* kp,
-                                     const ti64_icfg* cfg, int64_t lanes, int32_t init_bits,
-                                     void* stream) {
+static int64_t coupled_step_impl(const double* tn_d, double* tn1_d, const ti64_fields* f,
+                                 int64_t state_z0, uint32_t* idle_bits_d, uint32_t* scratch_d,
+                                 const ti64_thermal* tp, const ti64_stencil_args* a,
+                                 const ti64_kparams* kp, const ti64_icfg* cfg, int64_t lanes,
+                                 int32_t init_bits, void* stream, void* kin_stream) {
   if (!tn_d || !tn1_d || !f || !idle_bits_d || !tp || !a || !kp || !cfg || tn_d == tn1_d ||
       !a->all_built || a->losses_on || a->nx % 32 != 0 || a->nx < 1 || a->ny < 1 ||
       a->z_top != a->nz || a->z_begin < 0 || a->z_end > a->nz || a->z_begin > a->z_end ||
@@ -947,13 +946,22 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
     return TI64_EINVAL;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t kin = reinterpret_cast<cudaStream_t>(kin_stream);
   const int64_t plane = a->nx * a->ny;
   const int64_t c_lo = (a->z_begin - state_z0) * plane;  // state cells of the updated planes
   const int64_t c_hi = (a->z_end - state_z0) * plane;
   if (c_hi == c_lo) return TI64_OK;
-  if (init_bits)
+  if (init_bits) {
     idle_bits_init_kernel<<<(unsigned)(((c_hi - c_lo) / 32 + 255) / 256), 256, 0, st>>>(
         *f, idle_bits_d, c_lo, c_hi);
+    if (kin != st) {  // the kinetics stream reads the map
+      cudaEvent_t ev;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      cudaEventRecord(ev, st);
+      cudaStreamWaitEvent(kin, ev, 0);
+      cudaEventDestroy(ev);
+    }
+  }
   StencilConst c;
   c.inv_rch2 = a->dt / (tp->rho_c * a->h * a->h);
   c.inv_rch = a->dt / (tp->rho_c * a->h);
@@ -986,15 +994,26 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
     uint32_t* list = scratch_d + (nrows_state + 31) / 32 + 4;
     o.hot = hot;
     if (launch_built<2>(tn_d, tn1_d, *a, c, *f, idle_bits_d, o, nzu, zchunk, st)) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaMemsetAsync(count, 0, sizeof(unsigned int), st);
+      static int sms = 0;
+      if (sms == 0) {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sms = v;
+      }
+      if (kin != st) {  // the row kinetics follow the stencil on their own stream
+        cudaEvent_t ev;
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        cudaEventRecord(ev, st);
+        cudaStreamWaitEvent(kin, ev, 0);
+        cudaEventDestroy(ev);
+      }
+      cudaMemsetAsync(count, 0, sizeof(unsigned int), kin);
       const int64_t thr = (row_hi - row_lo + 3) / 4;
-      rows_scan_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(idle_bits_d, hot, row_lo,
-                                                                      row_hi, list, count);
-      rows_kinetics_kernel<<<(unsigned)(sms * 8), 128, 0, st>>>(tn_d, tn1_d, *f, idle_bits_d, o,
-                                                                list, count);
+      rows_scan_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, kin>>>(idle_bits_d, hot, row_lo,
+                                                                       row_hi, list, count);
+      rows_kinetics_kernel<<<(unsigned)(sms * 8), 128, 0, kin>>>(tn_d, tn1_d, *f, idle_bits_d, o,
+                                                                 list, count);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         ti64_set_error(std::string("ti64_coupled_step: ") + cudaGetErrorString(e));
@@ -1017,6 +1036,27 @@ extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti
   }
   ti64_set_error("");
   return TI64_OK;
+}
+
+extern "C" int64_t ti64_coupled_step(const double* tn_d, double* tn1_d, const ti64_fields* f,
+                                     int64_t state_z0, uint32_t* idle_bits_d,
+                                     uint32_t* scratch_d, const ti64_thermal* tp,
+                                     const ti64_stencil_args* a, const ti64_kparams* kp,
+                                     const ti64_icfg* cfg, int64_t lanes, int32_t init_bits,
+                                     void* stream) {
+  return coupled_step_impl(tn_d, tn1_d, f, state_z0, idle_bits_d, scratch_d, tp, a, kp, cfg, lanes,
+                           init_bits, stream, stream);
+}
+
+extern "C" int64_t ti64_coupled_step_streams(const double* tn_d, double* tn1_d,
+                                             const ti64_fields* f, int64_t state_z0,
+                                             uint32_t* idle_bits_d, uint32_t* scratch_d,
+                                             const ti64_thermal* tp, const ti64_stencil_args* a,
+                                             const ti64_kparams* kp, const ti64_icfg* cfg,
+                                             int64_t lanes, int32_t init_bits, void* stream,
+                                             void* kin_stream) {
+  return coupled_step_impl(tn_d, tn1_d, f, state_z0, idle_bits_d, scratch_d, tp, a, kp, cfg, lanes,
+                           init_bits, stream, kin_stream);
 }
 
 // _thermal_substeps (thermal.py:290-318): nsub stencil steps from src into

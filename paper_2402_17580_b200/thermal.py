@@ -282,11 +282,12 @@ class CoupledDomain:
         self._idle_bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
         self._bits_valid = False
         self._split_scratch = None  # the split step's row bitmap / list (allocated on use)
+        self._overlap = None  # third temperature buffer, second scratch, kinetics stream
         del np
 
     def run(self, n_steps, dt, beams, source, kinetics_params=None, integrator_config=None,
             thermal_params=DEFAULT_THERMAL, bottom=353.0, losses=False, n_lanes=8, fused=None,
-            split=True, graph=False):
+            split=True, graph=False, overlap=True):
         """n_steps coupled steps; beams[k] = (x, y, power, on) of step k.
 
         fused=True (default when nx % 32 == 0 and no losses) runs the device
@@ -296,7 +297,9 @@ class CoupledDomain:
         fused=False issues step_thermal + step_all per step like the reference.
         graph=True (fused path) reads each step's beam from a device table and
         replays a captured two-step CUDA graph (one host call per two steps;
-        same results)."""
+        same results).  overlap=True (split path, no graph) rotates three
+        temperature buffers and runs the row kinetics of step k on a second
+        stream beside the stencil of step k+1 (same results)."""
         from .batch import step_all
         from .integrator import IntegratorConfig
         from .kinetics import DEFAULT_PARAMS
@@ -314,10 +317,10 @@ class CoupledDomain:
                 self.step += 1
             return self
         return self._run_fused(n_steps, dt, beams, source, kp, cfg, thermal_params, bottom,
-                               n_lanes, split, graph)
+                               n_lanes, split, graph, overlap)
 
     def _run_fused(self, n_steps, dt, beams, source, kp, cfg, thermal_params, bottom, n_lanes,
-                   split=True, graph=False):
+                   split=True, graph=False, overlap=True):
         import ctypes as C
         from . import _abi, _lib
         lib = _lib.require()
@@ -347,6 +350,9 @@ class CoupledDomain:
             _lib.check(rc, "ti64_coupled_step")
             self._bits_valid = True
 
+        if split and overlap and not graph and n_steps >= 3:
+            return self._run_overlapped(n_steps, dt, beams, source, bottom, n_lanes, fs, tp, kpc,
+                                        cfgc)
         if graph and n_steps >= 3:
             import torch
             dev = self.fields.device
@@ -389,6 +395,52 @@ class CoupledDomain:
             self.fields.temperature_old.copy_(cur)
         else:
             self.fields.temperature_new.copy_(cur)
+        self.fields.traffic_bytes += 72 * self.fields.n_points * n_steps
+        self.fields.steps_taken += n_steps
+        return self
+
+
+    def _run_overlapped(self, n_steps, dt, beams, source, bottom, n_lanes, fs, tp, kpc, cfgc):
+        """The split coupled step with the row kinetics of step k on a second
+        stream beside the stencil of step k+1 (ti64_coupled_step_streams): three
+        temperature buffers in rotation, two scratch sets, one event per step
+        ordering stencil(k+2) behind kinetics(k)."""
+        import ctypes as C
+
+        import torch
+        from . import _abi, _lib
+        lib = _lib.require()
+        nz, ny, nx = self.shape
+        dev = self.fields.device
+        if self._overlap is None:
+            self._overlap = (torch.empty_like(self.fields.temperature_old),
+                             torch.zeros_like(self._split_scratch), torch.cuda.Stream(device=dev),
+                             [torch.cuda.Event() for _ in range(3)])
+        extra, scratch2, kin, events = self._overlap
+        main = torch.cuda.current_stream()
+        bufs = [self.fields.temperature_old, self.fields.temperature_new, extra]
+        scr = [_lib.ptr(self._split_scratch), _lib.ptr(scratch2)]
+        st, ks = _lib.stream_handle(main), _lib.stream_handle(kin)
+        kin.wait_stream(main)  # earlier work on the fields (and the idle bits) is done
+        for k in range(n_steps):
+            a = _abi.stencil_args(nx, ny, nz, nz, dt, self.field.h, beam=beams[k], source=source,
+                                  losses=False, bottom=bottom, all_built=True)
+            if k >= 2:
+                main.wait_event(events[(k - 2) % 3])  # kinetics(k-2) read B[(k+1) % 3]
+            rc = lib.ti64_coupled_step_streams(
+                _lib.ptr(bufs[k % 3]), _lib.ptr(bufs[(k + 1) % 3]), C.byref(fs), 0,
+                _lib.ptr(self._idle_bits), scr[k % 2], C.byref(tp), C.byref(a), C.byref(kpc),
+                C.byref(cfgc), int(n_lanes), 0 if self._bits_valid else 1, st, ks)
+            _lib.check(rc, "ti64_coupled_step_streams")
+            self._bits_valid = True
+            events[k % 3].record(kin)
+        main.wait_stream(kin)
+        final = bufs[n_steps % 3]
+        # the reference ends a step with temperature_old == temperature_new
+        for t in (self.fields.temperature_old, self.fields.temperature_new):
+            if t is not final:
+                t.copy_(final)
+        self.step += n_steps
         self.fields.traffic_bytes += 72 * self.fields.n_points * n_steps
         self.fields.steps_taken += n_steps
         return self
