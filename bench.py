@@ -696,9 +696,9 @@ def measure_ode(torch, pkg, cfg_id, K, W, rank, world, dev, dd, *, counted=True,
                       "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                       "path": "GlobalFields(device='host') + advance() -> ti64_advance_host: "
                               "the state lives in pinned host memory; chunks of 2^22 points are "
-                              "staged through three device buffers, the host->device copy of "
-                              "the next chunk and the device->host copy of the previous one "
-                              "overlapping each chunk's update; timed from the host arrays to "
+                              "staged through four device buffers, the host->device copies of "
+                              "the next chunks and the device->host copy of the previous one "
+                              "overlapping the chunks' updates; timed from the host arrays to "
                               "the phase sums and the updated host arrays",
                       "bitwise_equal_to_device_run": bool(same),
                       "seconds_per_step": t_e2e}
