@@ -16,6 +16,7 @@ import paper_2402_17580_b200 as pkg  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1 << 27)
 ap.add_argument("--windows", type=int, default=2)
+ap.add_argument("--window", type=int, default=200, help="steps per timed window")
 a = ap.parse_args()
 src = pkg.source_for_config(4)
 f = pkg.init_from_source(src, a.n)
@@ -26,12 +27,13 @@ while s < 20000:
     s += 5000
 pkg.advance(f, 200, src, step0=s, snapshot_every=200, scratch=scr)
 s += 200
+W = a.window
 for w in range(a.windows):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    pkg.advance(f, 200, src, step0=s, snapshot_every=200, scratch=scr)
+    pkg.advance(f, W, src, step0=s, snapshot_every=W, scratch=scr)
     e1.record()
     e1.synchronize()
-    s += 200
-    print(f"window {w}: steps {s - 200}-{s}: {e0.elapsed_time(e1):.2f} ms "
-          f"({a.n * 200 / e0.elapsed_time(e1) / 1e6:.3f} G upd/s)", flush=True)
+    s += W
+    print(f"window {w}: steps {s - W}-{s}: {e0.elapsed_time(e1):.2f} ms "
+          f"({a.n * W / e0.elapsed_time(e1) / 1e6:.3f} G upd/s)", flush=True)
