@@ -83,3 +83,21 @@ def test_error_path_without_device():
     rc = lib.ti64_run_range(C.byref(f), 0, 10, 3, 1, 1e-5, C.byref(kp), C.byref(cfg), 0,
                             None, None)
     assert rc == -1
+
+
+def test_host_staging_scratch_sizes_need_no_gpu():
+    """ti64_advance_host_scratch_bytes is host arithmetic: it grows with the
+    chunk size, covers four staged chunks of 50 B/point plus two advance
+    scratch sets, is independent of n once n exceeds the chunk, and rejects
+    negative sizes."""
+    lib = _lib.load()
+    f = lib.ti64_advance_host_scratch_bytes
+    adv = lib.ti64_advance_scratch_bytes
+    small, big = f(1 << 27, 1 << 20, 200, 200), f(1 << 27, 1 << 22, 200, 200)
+    assert 0 < small < big
+    assert big >= 4 * 50 * (1 << 22) + 2 * adv(1 << 22)
+    assert f(1 << 27, 0, 200, 200) == big                      # default chunk: 2^22 points
+    assert 0 <= big - f(1 << 26, 1 << 22, 200, 200) <= 512     # only the chunk-sum rows differ
+    assert f(1000, 1 << 22, 10, 0) < f(1 << 22, 1 << 22, 10, 0)  # chunk clipped to the input
+    assert f(-1, 0, 1, 0) < 0 and f(10, 0, -1, 0) < 0
+    assert adv(0) > 0 and adv(1 << 20) > adv(0)
